@@ -1,0 +1,1000 @@
+// Device code of libmt.so for sm_100a (B200).
+//
+//  * executor_kernel  -- the persistent stage executor: one cooperative launch,
+//    one CTA per SM; per stage every CTA pulls work tiles from its home tenant's operator queue
+//    (runtime-aware SM partition, a3) and, when that queue is empty or blocked, from the other
+//    tenants (round-robin, the device analogue of the paper's BFS issue); an op's tiles
+//    start only when its producers are complete ("operators in one stream can only be launched
+//    sequentially", P:289 -- relaxed to true data dependencies); a grid barrier ends each stage
+//    ("all operators in the same stage must all finish so as to step into the next stage").
+//  * tile functions   -- conv as implicit GEMM on tcgen05 (UMMA 128xBNx16, bf16 in, fp32 in TMEM)
+//    with a fused scale/shift/residual/activation epilogue (a5); depthwise conv (a6); pools,
+//    elementwise, input pack (a7); FC GEMV (a8).  The SAME tile functions run in the executor
+//    and in the one-launch-per-op baselines, so outputs are bit-identical across all schedules.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.h"
+#include "mt_types.h"
+
+namespace mtk {
+
+typedef __nv_bfloat16 bf16;
+
+// ------------------------------------------------------------------------------------------
+// shared-memory map of a CTA (1024-aligned base)
+// ------------------------------------------------------------------------------------------
+static constexpr int A_STAGE = MT_BM * MT_BK * 2;          // 16 KB: 128 rows x 128 B
+static constexpr int B_STAGE = 128 * MT_BK * 2;            // 16 KB: up to BN = 128 rows
+static constexpr int PIPE_BYTES = MT_STAGES * (A_STAGE + B_STAGE);
+static constexpr int TMEM_COLS = 128;
+
+struct CtaShared {
+  unsigned long long bar_empty[MT_STAGES];
+  unsigned long long bar_accf;
+  uint32_t tmem_base;
+  int op, tile, last, ok, home;
+  int cur[MT_MAXT], end[MT_MAXT];
+  OpDesc d;
+};
+static constexpr int SMEM_BYTES = 1024 + PIPE_BYTES + ((sizeof(CtaShared) + 127) / 128) * 128;
+
+struct PipeState {
+  uint32_t fill;       // k-blocks loaded so far by this CTA (stage ring position)
+  uint32_t acc_phase;  // parity of the accumulator-ready barrier
+};
+
+// ------------------------------------------------------------------------------------------
+// PTX helpers
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_u(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (bf16 inputs, fp32 accumulate), one CTA
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+// 32 lanes x 32 bit x 8 columns: thread i of the warp gets TMEM lane (base lane + i), 8 columns
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float *v) {
+  uint32_t r0, r1, r2, r3, r4, r5, r6, r7;
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3), "=r"(r4), "=r"(r5), "=r"(r6), "=r"(r7)
+      : "r"(taddr)
+      : "memory");
+  v[0] = __uint_as_float(r0); v[1] = __uint_as_float(r1); v[2] = __uint_as_float(r2);
+  v[3] = __uint_as_float(r3); v[4] = __uint_as_float(r4); v[5] = __uint_as_float(r5);
+  v[6] = __uint_as_float(r6); v[7] = __uint_as_float(r7);
+}
+// UMMA shared-memory descriptor: K-major operand, 128-byte swizzle, 8-row atoms of 1024 B
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);      // start address
+  d |= (uint64_t)(16 >> 4) << 16;              // leading byte offset (ignored for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;            // stride byte offset: next 8-row group
+  d |= (uint64_t)1 << 46;                      // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                      // SWIZZLE_128B
+  return d;
+}
+// instruction descriptor kind::f16: D f32, A/B bf16, both K-major, M = 128, N = n
+__device__ __forceinline__ uint32_t idesc_bf16(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(MT_BM >> 4) << 24);
+}
+
+// ------------------------------------------------------------------------------------------
+// element helpers: 8 channels at a time (16 B of bf16, 32 B of fp32)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void ld8_cg(const bf16 *p, float *v) {  // activations: L2 only
+  uint4 u;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "l"(p));
+  const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void ld8_cg(const float *p, float *v) {
+  float4 a, b;
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(p));
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w) : "l"(p + 4));
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void ld8_nc(const bf16 *p, float *v) {  // immutable weights
+  uint4 u = __ldg(reinterpret_cast<const uint4 *>(p));
+  const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void ld8_nc(const float *p, float *v) {
+  float4 a = __ldg(reinterpret_cast<const float4 *>(p)), b = __ldg(reinterpret_cast<const float4 *>(p + 4));
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void st8(bf16 *p, const float *v) {
+  uint4 u;
+  __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  *reinterpret_cast<uint4 *>(p) = u;
+}
+__device__ __forceinline__ void st8(float *p, const float *v) {
+  reinterpret_cast<float4 *>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4 *>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ float ld1_cg(const bf16 *p) {
+  unsigned short u;
+  asm volatile("ld.global.cg.u16 %0, [%1];" : "=h"(u) : "l"(p));
+  return __bfloat162float(__ushort_as_bfloat16(u));
+}
+__device__ __forceinline__ float ld1_cg(const float *p) { return __ldcg(p); }
+__device__ __forceinline__ void st1(bf16 *p, float v) { *p = __float2bfloat16_rn(v); }
+__device__ __forceinline__ void st1(float *p, float v) { *p = v; }
+
+__device__ __forceinline__ float act_f(float y, int act) {
+  if (act == 1) return fmaxf(y, 0.f);
+  if (act == 2) return fminf(fmaxf(y, 0.f), 6.f);
+  return y;
+}
+
+template <typename T>
+__device__ __forceinline__ const T *in_ptr(const RunArgs &a, const OpDesc &d) {
+  return (d.flags & OPF_GRAPH_IN) ? reinterpret_cast<const T *>(a.packed[d.tenant])
+                                  : reinterpret_cast<const T *>(d.in);
+}
+
+// store 8 output channels [c0, c0+8) of output pixel `pix` (row of N*Ho*Wo); nvalid <= 8
+template <typename T>
+__device__ __forceinline__ void store_out8(const RunArgs &a, const OpDesc &d, int64_t pix, int c0,
+                                           const float *v, int nvalid) {
+  if (d.flags & OPF_OUT) {
+    float *o = a.outputs[d.tenant] + pix * d.Co + c0;
+    for (int e = 0; e < nvalid; ++e) o[e] = v[e];
+  } else {
+    T *o = reinterpret_cast<T *>(d.out) + pix * d.out_cs + d.out_co + c0;
+    if (nvalid == 8) st8(o, v);
+    else
+      for (int e = 0; e < nvalid; ++e) st1(o + e, v[e]);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// a5: conv implicit GEMM on tcgen05.  GEMM view M = N*Ho*Wo (pixels), N = Cout, K = kh*kw*C
+// (K order (r, s, c), c fastest, matching NHWC).  A = im2col rows gathered with cp.async
+// (zero-fill for padding / tails), B = packed weights [Cout_pad][Kpad].  Both staged in a
+// MT_STAGES-deep ring of 128B-swizzled K-major tiles; one thread issues UMMA 128 x BN x 16 and
+// commits to per-stage mbarriers; the accumulator lives in TMEM and is drained by all 8 warps.
+// Deterministic split-K: fp32 partials in workspace, the last-arriving CTA sums them in split
+// order 0..S-1 and runs the epilogue.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void conv_epilogue_vals(const RunArgs &a, const OpDesc &d, int m, int n,
+                                                   float *v) {
+  const int nvalid = min(8, d.Co - n);
+  const float *sc = reinterpret_cast<const float *>(d.scale);
+  const float *sh = reinterpret_cast<const float *>(d.shift);
+  float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (d.flags & OPF_RES) {
+    const bf16 *rp = reinterpret_cast<const bf16 *>(d.res) + (int64_t)m * d.res_cs + d.res_co + n;
+    if (nvalid == 8) ld8_cg(rp, r);
+    else
+      for (int e = 0; e < nvalid; ++e) r[e] = ld1_cg(rp + e);
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    if (e < nvalid) v[e] = act_f(fmaf(v[e], __ldg(sc + n + e), __ldg(sh + n + e)) + r[e], d.act);
+  }
+  store_out8<bf16>(a, d, m, n, v, nvalid);
+}
+
+__device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_t *smem,
+                             CtaShared &sh, PipeState &ps) {
+  const int tid = threadIdx.x;
+  const int S = d.splits;
+  const int tmn = tile / S, ks = tile - tmn * S;
+  const int mt = tmn % d.tiles_m, nt = tmn / d.tiles_m;
+  const int m0 = mt * MT_BM, n0 = nt * d.bn;
+  const int kb0 = ks * d.kb_per_split;
+  const int kb1 = min(d.nkb, kb0 + d.kb_per_split);
+  const int nk = kb1 - kb0;
+  const bf16 *X = in_ptr<bf16>(a, d);
+  const bf16 *Wt = reinterpret_cast<const bf16 *>(d.w);
+  const int HoWo = d.Ho * d.Wo;
+  // per-thread im2col rows: r_i = (tid >> 3) + 32 i, 16-byte chunk c = tid & 7 of the K-block
+  const int c = tid & 7;
+  int pbase[4], hb[4], wb[4];
+  bool rv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + (tid >> 3) + 32 * i;
+    rv[i] = m < d.M;
+    const int mm = rv[i] ? m : 0;
+    const int n = mm / HoWo, rem = mm - n * HoWo;
+    const int ho = rem / d.Wo, wo = rem - ho * d.Wo;
+    pbase[i] = n * d.H * d.W;
+    hb[i] = ho * d.sh - d.ph;
+    wb[i] = wo * d.sw - d.pw;
+  }
+  const uint32_t sA = smem_u32(smem), sB = sA + MT_STAGES * A_STAGE;
+  const uint32_t idesc = idesc_bf16(d.bn);
+  const uint32_t tmem = sh.tmem_base;
+  const uint32_t bar_empty0 = smem_u32(&sh.bar_empty[0]);
+  const uint32_t bar_accf = smem_u32(&sh.bar_accf);
+
+  for (int i = 0; i < nk + MT_STAGES - 1; ++i) {
+    if (i < nk) {
+      const uint32_t f = ps.fill + i;
+      const int s = f % MT_STAGES;
+      if (f >= MT_STAGES) mbar_wait(bar_empty0 + 8 * s, ((f / MT_STAGES) - 1) & 1);
+      const int kb = kb0 + i;
+      const int k = kb * MT_BK + c * 8;
+      const bool kv = k < d.K;
+      const int tap = kv ? k / d.C : 0;
+      const int ci = k - tap * d.C;
+      const int rr = tap / d.kw, ss = tap - rr * d.kw;
+      const uint32_t sa = sA + s * A_STAGE;
+#pragma unroll
+      for (int i2 = 0; i2 < 4; ++i2) {
+        const int row = (tid >> 3) + 32 * i2;
+        const int hi = hb[i2] + rr, wi = wb[i2] + ss;
+        const bool valid = kv && rv[i2] && hi >= 0 && hi < d.H && wi >= 0 && wi < d.W;
+        const bf16 *src = valid ? X + (int64_t)(pbase[i2] + hi * d.W + wi) * d.in_cs + d.in_co + ci : X;
+        cp_async16(sa + row * 128 + ((c ^ (row & 7)) << 4), src, valid);
+      }
+      const uint32_t sb = sB + s * B_STAGE;
+      for (int row = tid >> 3; row < d.bn; row += 32) {
+        const bf16 *src = Wt + (int64_t)(n0 + row) * d.Kpad + kb * MT_BK + c * 8;
+        cp_async16(sb + row * 128 + ((c ^ (row & 7)) << 4), src, true);
+      }
+    }
+    cp_async_commit();
+    const int j = i - (MT_STAGES - 1);
+    if (j >= 0) {
+      cp_async_wait<MT_STAGES - 1>();
+      fence_proxy_async();  // make the cp.async smem writes visible to the tensor core (async proxy)
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        const int s = (ps.fill + j) % MT_STAGES;
+        const uint32_t ab = sA + s * A_STAGE, bb = sB + s * B_STAGE;
+#pragma unroll
+        for (int kk = 0; kk < MT_BK / 16; ++kk)
+          tc_mma(tmem, sdesc_sw128(ab + kk * 32), sdesc_sw128(bb + kk * 32), idesc,
+                 (j > 0 || kk > 0) ? 1u : 0u);
+        tc_commit(bar_empty0 + 8 * s);        // frees the smem stage when these MMAs complete
+        if (j == nk - 1) tc_commit(bar_accf);  // accumulator complete
+      }
+    }
+  }
+  ps.fill += nk;
+  mbar_wait(bar_accf, ps.acc_phase);
+  ps.acc_phase ^= 1;
+  tc_fence_after();
+
+  // epilogue: warp w drains TMEM lanes 32*(w&3).. and column half (w>>2)
+  const int warp = tid >> 5, lane = tid & 31;
+  const int q = warp & 3, half = warp >> 2;
+  const int r = 32 * q + lane;
+  const int m = m0 + r;
+  const int hcols = d.bn >> 1;
+  const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+  if (S == 1) {
+    for (int col = half * hcols; col < (half + 1) * hcols; col += 8) {
+      float v[8];
+      tmem_ld8(tl + col, v);
+      if (m < d.M && n0 + col < d.Co) conv_epilogue_vals(a, d, m, n0 + col, v);
+    }
+  } else {
+    float *ws = reinterpret_cast<float *>(d.ws);
+    for (int col = half * hcols; col < (half + 1) * hcols; col += 8) {
+      float v[8];
+      tmem_ld8(tl + col, v);
+      float *p = ws + ((int64_t)(tmn * S + ks) * d.bn + col) * MT_BM + r;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) __stcg(p + e * MT_BM, v[e]);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      const int old = atomicAdd(a.splitcnt + d.cnt_off + tmn, 1);
+      sh.last = (old == S - 1);
+      if (sh.last) {
+        a.splitcnt[d.cnt_off + tmn] = 0;  // ready for the next run
+        __threadfence();
+      }
+    }
+    __syncthreads();
+    if (sh.last) {
+      for (int col = half * hcols; col < (half + 1) * hcols; col += 8) {
+        float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int s2 = 0; s2 < S; ++s2) {  // fixed summation order: deterministic
+          const float *p = ws + ((int64_t)(tmn * S + s2) * d.bn + col) * MT_BM + r;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] += __ldcg(p + e * MT_BM);
+        }
+        if (m < d.M && n0 + col < d.Co) conv_epilogue_vals(a, d, m, n0 + col, v);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------------------------------
+// fp32 path (config 1, 1e-4 parity): implicit GEMM on CUDA cores, 64 x 64 tile, 4x4 per thread
+// ------------------------------------------------------------------------------------------
+template <typename T>
+__device__ void conv_simt_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_t *smem) {
+  float *As = reinterpret_cast<float *>(smem);                 // [BK][BM]
+  float *Bs = As + MT_SIMT_BK * MT_SIMT_BM;                    // [BK][BN]
+  const int tid = threadIdx.x;
+  const int mt = tile % d.tiles_m, nt = tile / d.tiles_m;
+  const int m0 = mt * MT_SIMT_BM, n0 = nt * MT_SIMT_BN;
+  const T *X = in_ptr<T>(a, d);
+  const float *Wt = reinterpret_cast<const float *>(d.w);
+  const int HoWo = d.Ho * d.Wo;
+  const int ty = tid >> 4, tx = tid & 15;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  for (int k0 = 0; k0 < d.K; k0 += MT_SIMT_BK) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + 256 * i;
+      const int kk = idx & 15, p = idx >> 4;
+      const int k = k0 + kk, m = m0 + p;
+      float v = 0.f;
+      if (k < d.K && m < d.M) {
+        const int tap = k / d.C, ci = k - tap * d.C;
+        const int rr = tap / d.kw, ss = tap - rr * d.kw;
+        const int n = m / HoWo, rem = m - n * HoWo;
+        const int ho = rem / d.Wo, wo = rem - ho * d.Wo;
+        const int hi = ho * d.sh - d.ph + rr, wi = wo * d.sw - d.pw + ss;
+        if (hi >= 0 && hi < d.H && wi >= 0 && wi < d.W)
+          v = ld1_cg(X + ((int64_t)(n * d.H + hi) * d.W + wi) * d.in_cs + d.in_co + ci);
+      }
+      As[kk * MT_SIMT_BM + p] = v;
+      const int co = n0 + p;
+      Bs[kk * MT_SIMT_BN + p] = (k < d.K && co < d.Co) ? __ldg(Wt + (int64_t)co * d.K + k) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < MT_SIMT_BK; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[kk * MT_SIMT_BM + ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk * MT_SIMT_BN + tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  const float *sc = reinterpret_cast<const float *>(d.scale);
+  const float *sf = reinterpret_cast<const float *>(d.shift);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= d.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= d.Co) continue;
+      float y = fmaf(acc[i][j], __ldg(sc + n), __ldg(sf + n));
+      if (d.flags & OPF_RES) y += ld1_cg(reinterpret_cast<const T *>(d.res) + (int64_t)m * d.res_cs + d.res_co + n);
+      y = act_f(y, d.act);
+      if (d.flags & OPF_OUT) a.outputs[d.tenant][(int64_t)m * d.Co + n] = y;
+      else st1(reinterpret_cast<T *>(d.out) + (int64_t)m * d.out_cs + d.out_co + n, y);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// a6: depthwise conv (+ folded BN + act); item = (output pixel, 8-channel group)
+// ------------------------------------------------------------------------------------------
+template <typename T>
+__device__ void dw_tile(const RunArgs &a, const OpDesc &d, int tile) {
+  const T *X = in_ptr<T>(a, d);
+  const T *Wt = reinterpret_cast<const T *>(d.w);
+  const int cg = d.C >> 3;
+  const int64_t items = (int64_t)d.N * d.Ho * d.Wo * cg;
+  const float *sc = reinterpret_cast<const float *>(d.scale);
+  const float *sf = reinterpret_cast<const float *>(d.shift);
+#pragma unroll
+  for (int e = 0; e < MT_EW_PER_THREAD; ++e) {
+    const int64_t it = (int64_t)tile * (MT_NTHREADS * MT_EW_PER_THREAD) + e * MT_NTHREADS + threadIdx.x;
+    if (it >= items) break;
+    const int64_t pix = it / cg;
+    const int g = (int)(it - pix * cg);
+    const int n = (int)(pix / (d.Ho * d.Wo));
+    const int rem = (int)(pix - (int64_t)n * d.Ho * d.Wo);
+    const int ho = rem / d.Wo, wo = rem - ho * d.Wo;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int r = 0; r < d.kh; ++r) {
+      const int hi = ho * d.sh - d.ph + r;
+      if (hi < 0 || hi >= d.H) continue;
+      for (int s = 0; s < d.kw; ++s) {
+        const int wi = wo * d.sw - d.pw + s;
+        if (wi < 0 || wi >= d.W) continue;
+        float x[8], w[8];
+        ld8_cg(X + ((int64_t)(n * d.H + hi) * d.W + wi) * d.in_cs + d.in_co + g * 8, x);
+        ld8_nc(Wt + (int64_t)(r * d.kw + s) * d.C + g * 8, w);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = fmaf(x[q], w[q], acc[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = act_f(fmaf(acc[q], __ldg(sc + g * 8 + q), __ldg(sf + g * 8 + q)), d.act);
+    store_out8<T>(a, d, pix, g * 8, acc, 8);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// a7: max / avg pooling (PyTorch window semantics: padding, ceil_mode, count_include_pad)
+// ------------------------------------------------------------------------------------------
+template <typename T>
+__device__ void pool_tile(const RunArgs &a, const OpDesc &d, int tile) {
+  const T *X = in_ptr<T>(a, d);
+  const int cg = d.C >> 3;
+  const int64_t items = (int64_t)d.N * d.Ho * d.Wo * cg;
+  const bool is_max = d.kind == 4;
+#pragma unroll
+  for (int e = 0; e < MT_EW_PER_THREAD; ++e) {
+    const int64_t it = (int64_t)tile * (MT_NTHREADS * MT_EW_PER_THREAD) + e * MT_NTHREADS + threadIdx.x;
+    if (it >= items) break;
+    const int64_t pix = it / cg;
+    const int g = (int)(it - pix * cg);
+    const int n = (int)(pix / (d.Ho * d.Wo));
+    const int rem = (int)(pix - (int64_t)n * d.Ho * d.Wo);
+    const int ho = rem / d.Wo, wo = rem - ho * d.Wo;
+    const int hs = ho * d.sh - d.ph, ws = wo * d.sw - d.pw;
+    const int he = min(hs + d.kh, d.H + d.ph), we = min(ws + d.kw, d.W + d.pw);
+    int div = (he - hs) * (we - ws);
+    const int h0 = max(hs, 0), h1 = min(he, d.H), w0 = max(ws, 0), w1 = min(we, d.W);
+    if (!d.cip) div = (h1 - h0) * (w1 - w0);
+    float acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = is_max ? -INFINITY : 0.f;
+    for (int hi = h0; hi < h1; ++hi)
+      for (int wi = w0; wi < w1; ++wi) {
+        float x[8];
+        ld8_cg(X + ((int64_t)(n * d.H + hi) * d.W + wi) * d.in_cs + d.in_co + g * 8, x);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = is_max ? fmaxf(acc[q], x[q]) : acc[q] + x[q];
+      }
+    if (!is_max) {
+      const float inv = 1.f / (float)div;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = acc[q] * inv;
+    }
+    store_out8<T>(a, d, pix, g * 8, acc, 8);
+  }
+}
+
+// global average pool; item = (n, 8-channel group)
+template <typename T>
+__device__ void gap_tile(const RunArgs &a, const OpDesc &d, int tile) {
+  const T *X = in_ptr<T>(a, d);
+  const int cg = d.C >> 3;
+  const int64_t it = (int64_t)tile * MT_NTHREADS + threadIdx.x;
+  if (it >= (int64_t)d.N * cg) return;
+  const int n = (int)(it / cg), g = (int)(it - (int64_t)n * cg);
+  const int HW = d.H * d.W;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const T *p = X + (int64_t)n * HW * d.in_cs + d.in_co + g * 8;
+  for (int i = 0; i < HW; ++i) {
+    float x[8];
+    ld8_cg(p + (int64_t)i * d.in_cs, x);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] += x[q];
+  }
+  const float inv = 1.f / (float)HW;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] *= inv;
+  store_out8<T>(a, d, n, g * 8, acc, 8);
+}
+
+// ------------------------------------------------------------------------------------------
+// a8: FC (GEMV at b=1, skinny GEMM up to 8 columns per pass): one warp per output row, 16-byte
+// weight loads, lane-strided partial sums reduced by a fixed xor-shuffle tree (deterministic)
+// ------------------------------------------------------------------------------------------
+template <typename T>
+__device__ void fc_tile(const RunArgs &a, const OpDesc &d, int tile) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rb = (int)(tile % ((d.Co + MT_FC_ROWS - 1) / MT_FC_ROWS));
+  const int bb = (int)(tile / ((d.Co + MT_FC_ROWS - 1) / MT_FC_ROWS));
+  const int o = rb * MT_FC_ROWS + warp;
+  if (o >= d.Co) return;
+  const int b0 = bb * MT_FC_BATCH;
+  const int nb = min(MT_FC_BATCH, d.N - b0);
+  const T *X = in_ptr<T>(a, d);
+  const T *Wr = reinterpret_cast<const T *>(d.w) + (int64_t)o * d.K;
+  const int K8 = d.K >> 3;
+  float acc[MT_FC_BATCH];
+#pragma unroll
+  for (int b = 0; b < MT_FC_BATCH; ++b) acc[b] = 0.f;
+#pragma unroll 4
+  for (int k8 = lane; k8 < K8; k8 += 32) {
+    float w[8];
+    ld8_nc(Wr + (int64_t)k8 * 8, w);
+#pragma unroll
+    for (int b = 0; b < MT_FC_BATCH; ++b) {
+      if (b < nb) {
+        float x[8];
+        ld8_cg(X + (int64_t)(b0 + b) * d.K + (int64_t)k8 * 8, x);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[b] = fmaf(w[q], x[q], acc[b]);
+      }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < MT_FC_BATCH; ++b) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], off);
+  }
+  if (lane == 0) {
+    const float sc = __ldg(reinterpret_cast<const float *>(d.scale) + o);
+    const float sf = __ldg(reinterpret_cast<const float *>(d.shift) + o);
+    for (int b = 0; b < nb; ++b) {
+      const float y = act_f(fmaf(acc[b], sc, sf), d.act);
+      if (d.flags & OPF_OUT) a.outputs[d.tenant][(int64_t)(b0 + b) * d.Co + o] = y;
+      else st1(reinterpret_cast<T *>(d.out) + (int64_t)(b0 + b) * d.out_cs + d.out_co + o, y);
+    }
+  }
+}
+
+// ADD (sum of inputs) / BN (affine) / RELU, + act
+template <typename T>
+__device__ void elt_tile(const RunArgs &a, const OpDesc &d, int tile) {
+  const int cg = d.Co >> 3;
+  const int64_t items = (int64_t)d.N * d.Ho * d.Wo * cg;
+#pragma unroll
+  for (int e = 0; e < MT_EW_PER_THREAD; ++e) {
+    const int64_t it = (int64_t)tile * (MT_NTHREADS * MT_EW_PER_THREAD) + e * MT_NTHREADS + threadIdx.x;
+    if (it >= items) break;
+    const int64_t pix = it / cg;
+    const int g = (int)(it - pix * cg);
+    float y[8];
+    if (d.kind == 8) {  // ADD
+      for (int q = 0; q < 8; ++q) y[q] = 0.f;
+      for (int i = 0; i < d.n_in; ++i) {
+        const T *p = d.ins[i] ? reinterpret_cast<const T *>(d.ins[i]) : reinterpret_cast<const T *>(a.packed[d.tenant]);
+        float x[8];
+        ld8_cg(p + pix * d.ins_cs[i] + d.ins_co[i] + g * 8, x);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) y[q] += x[q];
+      }
+    } else {
+      ld8_cg(in_ptr<T>(a, d) + pix * d.in_cs + d.in_co + g * 8, y);
+      if (d.kind == 2) {  // BN
+        const float *sc = reinterpret_cast<const float *>(d.scale);
+        const float *sf = reinterpret_cast<const float *>(d.shift);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) y[q] = fmaf(y[q], __ldg(sc + g * 8 + q), __ldg(sf + g * 8 + q));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = act_f(y[q], d.act);
+    store_out8<T>(a, d, pix, g * 8, y, 8);
+  }
+}
+
+// a7: input pack NCHW fp32 -> NHWC (bf16 or fp32), channels zero-padded to cpad (the
+// shared input is packed once per distinct pointer)
+template <typename T>
+__device__ void pack_pixels(const RunArgs &a, int t, int64_t first, int64_t stride) {
+  const int N = a.in_n[t], C = a.in_c[t], H = a.in_h[t], W = a.in_w[t], cp = a.in_cpad[t];
+  const int64_t HW = (int64_t)H * W, total = (int64_t)N * HW;
+  const float *src = a.inputs[t];
+  T *dst = reinterpret_cast<T *>(a.packed[t]);
+  for (int64_t p = first; p < total; p += stride) {
+    const int64_t n = p / HW, hw = p - n * HW;
+    for (int c0 = 0; c0 < cp; c0 += 8) {
+      float v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = (c0 + q < C) ? __ldg(src + (n * C + c0 + q) * HW + hw) : 0.f;
+      st8(dst + p * cp + c0, v);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// tile dispatch (shared by the executor and the per-op baseline kernels)
+// ------------------------------------------------------------------------------------------
+__device__ void run_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_t *smem, CtaShared &sh,
+                         PipeState &ps) {
+  const bool f32 = d.prec == 1;
+  switch (d.tk) {
+    case TK_CONV_TC: conv_tc_tile(a, d, tile, smem, sh, ps); return;
+    case TK_CONV_SIMT:
+      if (f32) conv_simt_tile<float>(a, d, tile, smem);
+      else conv_simt_tile<bf16>(a, d, tile, smem);
+      break;
+    case TK_DW: if (f32) dw_tile<float>(a, d, tile); else dw_tile<bf16>(a, d, tile); break;
+    case TK_POOL: if (f32) pool_tile<float>(a, d, tile); else pool_tile<bf16>(a, d, tile); break;
+    case TK_GAP: if (f32) gap_tile<float>(a, d, tile); else gap_tile<bf16>(a, d, tile); break;
+    case TK_FC: if (f32) fc_tile<float>(a, d, tile); else fc_tile<bf16>(a, d, tile); break;
+    case TK_ELT: if (f32) elt_tile<float>(a, d, tile); else elt_tile<bf16>(a, d, tile); break;
+    default: break;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void load_desc(CtaShared &sh, const OpDesc *src) {
+  const int *s = reinterpret_cast<const int *>(src);
+  int *d = reinterpret_cast<int *>(&sh.d);
+  for (int i = threadIdx.x; i < (int)(sizeof(OpDesc) / 4); i += blockDim.x) d[i] = __ldg(s + i);
+}
+
+__device__ __forceinline__ uint8_t *smem_base() {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  return reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+}
+
+__device__ void cta_setup(CtaShared &sh, bool need_tmem) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < MT_STAGES; ++s) mbar_init(smem_u32(&sh.bar_empty[s]), 1);
+    mbar_init(smem_u32(&sh.bar_accf), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (need_tmem && (tid >> 5) == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sh.tmem_base)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+}
+
+__device__ void cta_teardown(CtaShared &sh, bool need_tmem) {
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (need_tmem && (threadIdx.x >> 5) == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sh.tmem_base), "r"(TMEM_COLS)
+                 : "memory");
+}
+
+// ------------------------------------------------------------------------------------------
+// grid barrier (sense via a generation counter; all CTAs co-resident by cooperative launch)
+// ------------------------------------------------------------------------------------------
+__device__ bool grid_barrier(const RunArgs &a, CtaShared &sh) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    CtlBlock *ctl = a.ctl;
+    const unsigned gen = ld_acquire_u(&ctl->bar_gen);
+    __threadfence();
+    const unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
+    int ok = 1;
+    if (arrived == gridDim.x - 1) {
+      atomicExch(&ctl->bar_count, 0u);
+      __threadfence();
+      st_release_u(&ctl->bar_gen, gen + 1);
+    } else {
+      const unsigned long long t0 = gtimer();
+      while (ld_acquire_u(&ctl->bar_gen) == gen) {
+        if (ld_acquire_u(&ctl->error)) { ok = 0; break; }
+        if (gtimer() - t0 > a.timeout_ns) {
+          atomicExch(&ctl->error, 1u);
+          ok = 0;
+          break;
+        }
+        __nanosleep(32);
+      }
+    }
+    sh.ok = ok;
+  }
+  __syncthreads();
+  return sh.ok != 0;
+}
+
+// one stage: pick (op, tile) from the home tenant first, then the others; returns false on abort
+__device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh, PipeState &ps) {
+  const int T = a.n_tenants;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int t = 0; t < T; ++t) {
+      sh.cur[t] = a.rng[(s * T + t) * 2];
+      sh.end[t] = a.rng[(s * T + t) * 2 + 1];
+    }
+    sh.home = a.home[(size_t)s * gridDim.x + blockIdx.x];
+  }
+  __syncthreads();
+  while (true) {
+    if (tid == 0) {
+      int op = -1, tile = 0, status = 0;  // status: 0 searching, 1 found, 2 stage exhausted, 3 abort
+      const unsigned long long t0 = gtimer();
+      unsigned spins = 0;
+      while (status == 0) {
+        bool all_done = true;
+        for (int q = 0; q < T && status == 0; ++q) {
+          if (!a.steal && q > 0) break;
+          const int t = (sh.home + q) % T;
+          while (sh.cur[t] < sh.end[t]) {
+            const int o = sh.cur[t];
+            const OpDesc *od = a.ops + o;
+            const int nd = __ldg(&od->n_dep);
+            bool ready = true;
+            for (int k = 0; k < nd; ++k) {
+              const int dep = __ldg(&od->deps[k]);
+              if (ld_acquire(a.done + dep) < __ldg(&od->dep_tiles[k])) { ready = false; break; }
+            }
+            if (!ready) { all_done = false; break; }  // tenant blocked on its chain
+            const int k = atomicAdd(a.claim + o, 1);
+            if (k < __ldg(&od->tiles)) { op = o; tile = k; status = 1; break; }
+            sh.cur[t] = o + 1;  // every tile of o claimed
+          }
+          if (status == 0 && sh.cur[t] < sh.end[t]) all_done = false;
+        }
+        if (status == 0 && all_done) status = 2;
+        if (status == 0) {
+          if ((++spins & 63) == 0) {
+            if (ld_acquire_u(&a.ctl->error)) status = 3;
+            else if (gtimer() - t0 > a.timeout_ns) { atomicExch(&a.ctl->error, 2u); status = 3; }
+          }
+          if (status == 0) __nanosleep(40);
+        }
+      }
+      sh.op = status == 1 ? op : (status == 2 ? -1 : -2);
+      sh.tile = tile;
+    }
+    __syncthreads();
+    const int op = sh.op;
+    if (op == -1) return true;
+    if (op == -2) return false;
+    load_desc(sh, a.ops + op);
+    __syncthreads();
+    run_tile(a, sh.d, sh.tile, smem, sh, ps);
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(a.done + op, 1);  // release: this tile's outputs are visible
+    }
+  }
+}
+
+__global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
+  uint8_t *smem = smem_base();
+  CtaShared &sh = *reinterpret_cast<CtaShared *>(smem + PIPE_BYTES);
+  PipeState ps{0u, 0u};
+  cta_setup(sh, true);
+  bool ok = grid_barrier(a, sh);
+  if (ok) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.ts) a.ts[0] = gtimer();
+    // prologue: pack every distinct graph input (grid-stride over all threads)
+    const int64_t first = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int q = 0; q < a.n_pack; ++q) {
+      const int t = a.pack_tenant[q];
+      if (a.in_prec[t] == 1) pack_pixels<float>(a, t, first, stride);
+      else pack_pixels<bf16>(a, t, first, stride);
+    }
+    ok = grid_barrier(a, sh);
+    if (ok && blockIdx.x == 0 && threadIdx.x == 0 && a.ts && a.ts_full) a.ts[2] = gtimer();
+  }
+  for (int s = 0; ok && s < a.n_stages; ++s) {
+    ok = run_stage(a, s, smem, sh, ps);
+    if (ok) ok = grid_barrier(a, sh);
+    if (ok && blockIdx.x == 0 && threadIdx.x == 0 && a.ts && a.ts_full) a.ts[3 + s] = gtimer();
+  }
+  if (ok) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.ts) a.ts[1] = gtimer();
+    // all tiles of the run are complete: reset the claim / done counters for the next launch
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ops; i += gridDim.x * blockDim.x) {
+      a.claim[i] = 0;
+      a.done[i] = 0;
+    }
+  }
+  cta_teardown(sh, true);
+}
+
+// baseline: all tiles of one op, grid-strided
+__global__ void __launch_bounds__(MT_NTHREADS, 1) op_kernel(RunArgs a, int op) {
+  uint8_t *smem = smem_base();
+  CtaShared &sh = *reinterpret_cast<CtaShared *>(smem + PIPE_BYTES);
+  PipeState ps{0u, 0u};
+  load_desc(sh, a.ops + op);
+  const bool tc = __ldg(&a.ops[op].tk) == TK_CONV_TC;
+  cta_setup(sh, tc);
+  for (int t = blockIdx.x; t < sh.d.tiles; t += gridDim.x) run_tile(a, sh.d, t, smem, sh, ps);
+  cta_teardown(sh, tc);
+}
+
+// small-smem variant for non-tensor-core ops so several op kernels can share an SM
+static constexpr int SMALL_SMEM = 1024 + MT_SIMT_BK * (MT_SIMT_BM + MT_SIMT_BN) * 4 + ((sizeof(CtaShared) + 127) / 128) * 128;
+__global__ void __launch_bounds__(MT_NTHREADS) op_kernel_small(RunArgs a, int op) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  CtaShared &sh = *reinterpret_cast<CtaShared *>(smem + MT_SIMT_BK * (MT_SIMT_BM + MT_SIMT_BN) * 4);
+  PipeState ps{0u, 0u};
+  load_desc(sh, a.ops + op);
+  __syncthreads();
+  for (int t = blockIdx.x; t < sh.d.tiles; t += gridDim.x) run_tile(a, sh.d, t, smem, sh, ps);
+}
+
+__global__ void pack_kernel(RunArgs a, int t) {
+  const int64_t first = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (a.in_prec[t] == 1) pack_pixels<float>(a, t, first, stride);
+  else pack_pixels<bf16>(a, t, first, stride);
+}
+
+// bind-time weight repack from the caller's fp32 PyTorch layouts
+__global__ void weight_pack_kernel(int mode, const float *src, void *dst, OpDesc d, int cin_real) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (mode == 1 || mode == 2) {  // conv [Cout][Cin][kh][kw] -> [rows][K] with K = (r, s, c)
+    const int rows = mode == 1 ? d.tiles_n * d.bn : d.Co;
+    const int ld = mode == 1 ? d.Kpad : d.K;
+    const int64_t total = (int64_t)rows * ld;
+    for (int64_t i = tid; i < total; i += stride) {
+      const int row = (int)(i / ld), k = (int)(i - (int64_t)row * ld);
+      float v = 0.f;
+      if (row < d.Co && k < d.K) {
+        const int tap = k / d.C, ci = k - tap * d.C;
+        const int r = tap / d.kw, s = tap - r * d.kw;
+        if (ci < cin_real) v = src[(((int64_t)row * cin_real + ci) * d.kh + r) * d.kw + s];
+      }
+      if (mode == 1) reinterpret_cast<bf16 *>(dst)[i] = __float2bfloat16_rn(v);
+      else reinterpret_cast<float *>(dst)[i] = v;
+    }
+  } else if (mode == 3) {  // depthwise [C][1][kh][kw] -> [kh*kw][C]
+    const int64_t total = (int64_t)d.kh * d.kw * d.C;
+    for (int64_t i = tid; i < total; i += stride) {
+      const int tap = (int)(i / d.C), ch = (int)(i - (int64_t)tap * d.C);
+      const float v = src[(int64_t)ch * d.kh * d.kw + tap];
+      if (d.prec == 0) reinterpret_cast<bf16 *>(dst)[i] = __float2bfloat16_rn(v);
+      else reinterpret_cast<float *>(dst)[i] = v;
+    }
+  } else if (mode == 4) {  // FC [out][C*H*W] (NCHW flatten) -> [out][H*W*C] (NHWC flatten)
+    const int64_t total = (int64_t)d.Co * d.K;
+    const int HW = d.H * d.W;
+    for (int64_t i = tid; i < total; i += stride) {
+      const int row = (int)(i / d.K), k = (int)(i - (int64_t)row * d.K);
+      const int pix = k / d.C, ci = k - pix * d.C;
+      float v = 0.f;
+      if (ci < cin_real) v = src[(int64_t)row * cin_real * HW + (int64_t)ci * HW + pix];
+      if (d.prec == 0) reinterpret_cast<bf16 *>(dst)[i] = __float2bfloat16_rn(v);
+      else reinterpret_cast<float *>(dst)[i] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// host launchers
+// ------------------------------------------------------------------------------------------
+size_t executor_smem_bytes() { return SMEM_BYTES; }
+
+static cudaError_t set_attrs() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(executor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(op_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  done = true;
+  return cudaSuccess;
+}
+
+cudaError_t executor_occupancy(int *bps) {
+  cudaError_t e = set_attrs();
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, executor_kernel, MT_NTHREADS, SMEM_BYTES);
+}
+
+cudaError_t launch_executor(const RunArgs &a, int grid, cudaStream_t s) {
+  cudaError_t e = set_attrs();
+  if (e != cudaSuccess) return e;
+  void *args[] = {(void *)&a};
+  return cudaLaunchCooperativeKernel((void *)executor_kernel, dim3(grid), dim3(MT_NTHREADS), args,
+                                     SMEM_BYTES, s);
+}
+
+cudaError_t launch_op(const RunArgs &a, const OpDesc &d, int op, int max_grid, cudaStream_t s) {
+  cudaError_t e = set_attrs();
+  if (e != cudaSuccess) return e;
+  if (d.tk == TK_CONV_TC) {
+    const int grid = d.tiles < max_grid ? d.tiles : max_grid;
+    op_kernel<<<grid, MT_NTHREADS, SMEM_BYTES, s>>>(a, op);
+  } else {
+    const int cap = 4 * max_grid;
+    const int grid = d.tiles < cap ? d.tiles : cap;
+    op_kernel_small<<<grid, MT_NTHREADS, SMALL_SMEM, s>>>(a, op);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack(const RunArgs &a, int t, cudaStream_t s) {
+  const int64_t pix = (int64_t)a.in_n[t] * a.in_h[t] * a.in_w[t];
+  int grid = (int)((pix + 255) / 256);
+  if (grid > 1184) grid = 1184;
+  pack_kernel<<<grid, 256, 0, s>>>(a, t);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_weight_pack(int mode, const float *src, void *dst, const OpDesc &d, int cin_real,
+                               cudaStream_t s) {
+  weight_pack_kernel<<<1184, 256, 0, s>>>(mode, src, dst, d, cin_real);
+  return cudaGetLastError();
+}
+
+}  // namespace mtk

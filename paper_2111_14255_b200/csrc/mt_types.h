@@ -1,0 +1,82 @@
+// Plan structures shared by the host plan compiler (plan.cpp) and the device code (kernels.cu).
+// Plain-old-data only: uploaded to device memory as-is.
+#pragma once
+#include <stdint.h>
+
+#define MT_MAXT 16        // max tenants (== MT_MAX_TENANTS)
+#define MT_MAXIN 8        // max inputs of one op (== MT_MAX_INPUTS)
+#define MT_MAXDEP 9       // inputs + residual
+#define MT_NTHREADS 256   // threads per CTA of every kernel
+#define MT_STAGES 4       // smem pipeline depth of the tcgen05 conv tile
+#define MT_BM 128         // tcgen05 conv tile rows (output pixels), UMMA M
+#define MT_BK 64          // K per pipeline stage (one 128-byte swizzle atom of bf16)
+#define MT_SIMT_BM 64     // SIMT conv tile
+#define MT_SIMT_BN 64
+#define MT_SIMT_BK 16
+#define MT_EW_PER_THREAD 2   // 8-channel vectors per thread in pointwise tiles
+#define MT_FC_ROWS 8         // FC output rows per tile (one per warp)
+#define MT_FC_BATCH 8        // FC batch columns per pass
+
+enum mt_tile_kind {
+  TK_NONE = 0,
+  TK_CONV_TC = 1,   // bf16 implicit GEMM on tcgen05 (UMMA 128 x BN x 16, fp32 accum in TMEM)
+  TK_CONV_SIMT = 2, // fp32-accumulating implicit GEMM on CUDA cores (fp32 graphs)
+  TK_DW = 3,        // depthwise conv on CUDA cores
+  TK_POOL = 4,      // max / avg pooling
+  TK_GAP = 5,       // global average pooling
+  TK_FC = 6,        // GEMV / skinny GEMM (weight streaming)
+  TK_ELT = 7        // ADD / BN / RELU
+};
+
+enum mt_op_flags {
+  OPF_OUT = 1,          // final op: writes fp32 into the caller's output buffer
+  OPF_RES = 2,          // fused residual
+  OPF_GRAPH_IN = 4,     // reads the (packed) graph input of its tenant
+};
+
+struct OpDesc {
+  int32_t kind, tk, tenant, prec;   // prec: 0 bf16, 1 fp32 storage
+  int32_t flags, act, n_in, n_dep;
+  int32_t N, H, W, C;               // input: batch, height, width, channels (stored, padded)
+  int32_t Ho, Wo, Co, groups;
+  int32_t kh, kw, sh, sw;
+  int32_t ph, pw, ceil_mode, cip;
+  int32_t in_cs, in_co, out_cs, out_co;
+  int32_t res_cs, res_co, ins_cs[MT_MAXIN], ins_co[MT_MAXIN];
+  int32_t deps[MT_MAXDEP];          // global op ids this op reads
+  int32_t dep_tiles[MT_MAXDEP];     // tile counts of those ops (dependency satisfied when done == tiles)
+  int32_t pad1;
+  int32_t M, K, Kpad, nkb;          // GEMM view (conv / FC)
+  int32_t bn, tiles_m, tiles_n, splits;
+  int32_t kb_per_split, tiles, cnt_off, pad0;
+  uint64_t in, res, out, w, scale, shift, ws;   // device addresses (filled at bind)
+  uint64_t ins[MT_MAXIN];                        // ADD inputs
+};
+
+// Device-side control block in the workspace (counters are zero between runs).
+struct CtlBlock {
+  unsigned int bar_count;
+  unsigned int bar_gen;
+  unsigned int error;        // nonzero: a spin timed out / invariant broken
+  unsigned int pad;
+  unsigned long long err_info;
+};
+
+struct RunArgs {
+  const OpDesc *ops;
+  const int32_t *rng;        // [S][T][2] global op ids (begin, end)
+  const uint8_t *home;       // [S][grid] home tenant of each CTA
+  int32_t n_stages, n_tenants, steal, n_pack;
+  int32_t *claim;            // [n_ops] tile claim counters
+  int32_t *done;             // [n_ops] finished-tile counters
+  int32_t *splitcnt;         // split-K arrival counters
+  CtlBlock *ctl;
+  unsigned long long *ts;    // [n_stages + 2] %globaltimer stamps (or NULL)
+  unsigned long long timeout_ns;
+  int32_t n_ops, ts_full;     // ts_full: 1 = all stage stamps, 0 = start/end only
+  const float *inputs[MT_MAXT];     // per tenant user input (NCHW fp32)
+  float *outputs[MT_MAXT];          // per tenant user output (fp32)
+  uint64_t packed[MT_MAXT];         // per tenant packed-input buffer (NHWC, C padded)
+  int32_t pack_tenant[MT_MAXT];     // tenants whose input is packed in the prologue
+  int32_t in_n[MT_MAXT], in_c[MT_MAXT], in_h[MT_MAXT], in_w[MT_MAXT], in_cpad[MT_MAXT], in_prec[MT_MAXT];
+};

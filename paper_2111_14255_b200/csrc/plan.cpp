@@ -1,0 +1,97 @@
+// Schedule IR (a2) and runtime-aware SM partition (a3) -- pure host functions.
+//
+// These restate the paper's IR (§3.2): Eq.3 pointer split, Eq.4/5 stages
+// with possibly empty ("None") slices, Eq.6 schedule, Eq.8 T(G, rho)
+// (P:386-393).  Semantics must equal oracle/ir.py bit for bit (tests/test_ir_parity.py); the
+// two implementations share no code.
+#include "plan.h"
+
+namespace mt {
+
+static mt_error_info E(int code, int s, int t, int op) { return mt_error_info{code, s, t, op}; }
+
+// First violation, scanning stages k = 0..S-1, tenants i = 0..N-1 (R1-R4).
+mt_error_info validate(const std::vector<int> &L, int S, const int32_t *r) {
+  const int N = (int)L.size();
+  if (S < 1) return E(MT_E_SHAPE, -1, -1, -1);
+  std::vector<int> pos(N, 0);
+  for (int k = 0; k < S; ++k) {
+    bool all_empty = true;
+    for (int i = 0; i < N; ++i) {
+      const int b = r[(k * N + i) * 2 + 0], e = r[(k * N + i) * 2 + 1];
+      if (b < 0 || e > L[i] || b > e) return E(MT_E_RANGE, k, i, b);
+      if (b != pos[i]) return E(MT_E_NONCONTIG, k, i, pos[i]);
+      if (e > b) all_empty = false;
+      pos[i] = e;
+    }
+    if (all_empty) return E(MT_E_EMPTY_STAGE, k, -1, -1);
+  }
+  for (int i = 0; i < N; ++i)
+    if (pos[i] != L[i]) return E(MT_E_INCOMPLETE, S, i, pos[i]);
+  return E(MT_E_OK, -1, -1, -1);
+}
+
+// tau = T(G, rho): stage k slice of tenant i = [rho_i[k-1], rho_i[k]), rho_i[-1] = 0,
+// rho_i[P] = L_i (Eq.3: (3,5,7) on 10 ops -> [1..3],[4,5],[6,7],[8..10]).
+mt_error_info pointers_to_ranges(const std::vector<int> &L, int P, const int32_t *rho,
+                                 std::vector<int32_t> &ranges) {
+  const int N = (int)L.size();
+  if (P < 0) return E(MT_E_SHAPE, -1, -1, -1);
+  for (int i = 0; i < N; ++i) {
+    int prev = 0;
+    for (int k = 0; k < P; ++k) {
+      const int p = rho[i * P + k];
+      if (p < 0 || p > L[i]) return E(MT_E_ROW_RANGE, k, i, p);
+      if (p < prev) return E(MT_E_ROW_ORDER, k, i, p);
+      prev = p;
+    }
+  }
+  const int S = P + 1;
+  ranges.assign((size_t)S * N * 2, 0);
+  for (int k = 0; k < S; ++k)
+    for (int i = 0; i < N; ++i) {
+      ranges[(k * N + i) * 2 + 0] = k == 0 ? 0 : rho[i * P + k - 1];
+      ranges[(k * N + i) * 2 + 1] = k == P ? L[i] : rho[i * P + k];
+    }
+  return validate(L, S, ranges.data());
+}
+
+// n_t proportional to w_t by largest remainder; every active tenant gets >= 1 CTA; ties in the
+// remainder go to the lower tenant index; inactive tenants get 0; all weights 0 -> equal.
+std::vector<int> sm_partition(const std::vector<bool> &active, const std::vector<__int128> &w,
+                              int n_sms) {
+  const int N = (int)active.size();
+  std::vector<int> out(N, 0);
+  int A = 0;
+  __int128 W = 0;
+  for (int t = 0; t < N; ++t)
+    if (active[t]) { ++A; W += w[t]; }
+  if (A == 0) return out;
+  std::vector<__int128> ww(N, 0);
+  for (int t = 0; t < N; ++t) ww[t] = active[t] ? (W == 0 ? (__int128)1 : w[t]) : 0;
+  if (W == 0) W = A;
+  const __int128 R = n_sms - A;
+  std::vector<__int128> rem(N, 0);
+  __int128 used = 0;
+  for (int t = 0; t < N; ++t) {
+    if (!active[t]) continue;
+    const __int128 q = R * ww[t] / W;
+    rem[t] = R * ww[t] % W;
+    out[t] = 1 + (int)q;
+    used += q;
+  }
+  int left = (int)(R - used);
+  std::vector<int> order;
+  for (int t = 0; t < N; ++t)
+    if (active[t]) order.push_back(t);
+  // stable selection: descending remainder, ascending index
+  for (int a = 0; a < (int)order.size(); ++a)
+    for (int b = a + 1; b < (int)order.size(); ++b) {
+      const int x = order[a], y = order[b];
+      if (rem[y] > rem[x] || (rem[y] == rem[x] && y < x)) { order[a] = y; order[b] = x; }
+    }
+  for (int k = 0; k < left && k < (int)order.size(); ++k) out[order[k]] += 1;
+  return out;
+}
+
+}  // namespace mt

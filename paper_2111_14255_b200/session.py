@@ -1,0 +1,61 @@
+"""Torch plumbing around the C ABI: device memory for parameters, workspace, inputs, outputs.
+
+No method logic lives here: graphs come from `workloads`, every computation runs in libmt.so.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .mt import Context
+
+
+class TenantMix:
+    """N tenant graphs loaded into one mt_ctx on a CUDA device, weights resident in HBM."""
+
+    def __init__(self, graphs, device=0, steal=True):
+        self.graphs = graphs
+        self.dev = torch.device("cuda", device)
+        self.ctx = Context(device)
+        if not steal:
+            self.ctx.set_option(1, 0)
+        self._params = []
+        ptrs = []
+        for g in graphs:
+            row = []
+            for j, nd in enumerate(g.nodes):
+                p = g.params[j]
+                if not p:
+                    row.append(None)
+                    continue
+                t = {k: torch.from_numpy(np.ascontiguousarray(v)).to(self.dev) for k, v in p.items()}
+                self._params.append(t)
+                row.append((t["weight"].data_ptr() if "weight" in t else None,
+                            t["scale"].data_ptr(), t["shift"].data_ptr()))
+            ptrs.append(row)
+        self.ctx.load_graphs(graphs, ptrs)
+        self.ws_bytes = self.ctx.workspace_size()
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.dev)
+        self.ctx.bind_workspace(self.ws.data_ptr(), self.ws_bytes)
+        self.outputs = [torch.empty((g.batch, g.out_classes), dtype=torch.float32, device=self.dev)
+                        for g in graphs]
+
+    def set_input(self, x_nchw):
+        """one shared input tensor for every tenant; returns the device pointers"""
+        self.x = torch.as_tensor(x_nchw, dtype=torch.float32).to(self.dev).contiguous()
+        return [self.x.data_ptr()] * len(self.graphs)
+
+    @property
+    def in_ptrs(self):
+        return [self.x.data_ptr()] * len(self.graphs)
+
+    @property
+    def out_ptrs(self):
+        return [o.data_ptr() for o in self.outputs]
+
+    def run(self, stream=0):
+        return self.ctx.run(self.in_ptrs, self.out_ptrs, stream)
+
+    def outputs_numpy(self):
+        torch.cuda.synchronize(self.dev)
+        return [o.cpu().numpy() for o in self.outputs]

@@ -1,0 +1,194 @@
+"""C-ABI library on the CPU box: loads, exports every declared symbol, and its host-side plan
+compiler (a1-a3) agrees bit for bit with the IR oracle (host-only contexts, no CUDA call)."""
+import ctypes as C
+import itertools
+import random
+
+import numpy as np
+import pytest
+
+from oracle import ir
+from workloads import configs, zoo
+
+mt = pytest.importorskip("paper_2111_14255_b200.mt")
+
+FAKE = (0x1000, 0x2000, 0x3000)   # host-only contexts never dereference parameter pointers
+
+
+def host_ctx(graphs, n_sms=148):
+    c = mt.Context(-1)
+    c.set_option(mt.MT_OPT_NUM_SMS, n_sms)
+    c.load_graphs(graphs, [[FAKE if g.params[j] else None for j in range(g.n_ops)] for g in graphs])
+    return c
+
+
+def test_exports_every_declared_symbol():
+    names = mt.declared_functions()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(mt.lib, n), n
+    assert b"sm_100a" in mt.mt_version()
+
+
+def test_elf_contains_sm100a_tcgen05_code():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", mt.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+    assert "UTCHMMA" in out or "UTCMMA" in out          # tcgen05.mma
+    assert "LDTM" in out                                  # tcgen05.ld
+
+
+def _tiny_graph(L):
+    """a chain of L eltwise ops (8 channels) for IR tests at arbitrary lengths"""
+    b = zoo.GraphBuilder("tinyA", 1, 8, 4, 4, zoo.PREC_FP32, seed=0)
+    x = -1
+    for _ in range(L):
+        x = b.relu(x)
+    return b.build()
+
+
+@pytest.mark.parametrize("lengths", [(3, 2), (2, 2, 1), (6, 6)])
+def test_validation_bit_exact_on_full_enumeration(lengths):
+    c = host_ctx([_tiny_graph(L) for L in lengths])
+    sch = ir.enumerate_schedules(lengths) if lengths != (6, 6) else None
+    if sch is None:   # (6,6): 287,648 schedules -- check a deterministic 3000-sample + count
+        assert ir.count_schedules(lengths) == 287648
+        rnd = random.Random(0)
+        full = ir.enumerate_schedules((6, 6))
+        sch = rnd.sample(full, 3000)
+    for s in sch:
+        c.set_schedule(s)
+        assert c.num_stages() == len(s)
+        so = c.stage_assignment()
+        assert so == ir.stage_of(lengths, s)
+
+
+def _mutations(lengths, rnd, n):
+    out = []
+    base = ir.enumerate_schedules(lengths)
+    for _ in range(n):
+        s = [list(map(list, st)) for st in rnd.choice(base)]
+        kind = rnd.randrange(7)
+        k = rnd.randrange(len(s))
+        i = rnd.randrange(len(lengths))
+        if kind == 0:
+            s[k][i][1] += rnd.choice([-1, 1])           # overlap / gap / range
+        elif kind == 1:
+            s[k][i][0] += rnd.choice([-1, 1])
+        elif kind == 2 and len(s) > 1:
+            s[0], s[-1] = s[-1], s[0]                  # reordered stages
+        elif kind == 3:
+            s.insert(k, [[st[0], st[0]] for st in s[k]])   # all-empty stage
+        elif kind == 4:
+            s = s[:-1] if len(s) > 1 else s            # missing ops
+        elif kind == 5:
+            s[k] = s[k][:-1]                           # wrong N
+        else:
+            s[k][i] = [s[k][i][1], s[k][i][0]]         # begin > end
+        out.append(s)
+    return out
+
+
+def test_validation_errors_bit_exact_on_mutated_corpus():
+    lengths = (3, 4, 2)
+    c = host_ctx([_tiny_graph(L) for L in lengths])
+    rnd = random.Random(7)
+    n_err = 0
+    for s in _mutations(lengths, rnd, 3000):
+        if any(len(st) != len(lengths) for st in s):
+            exp = (ir.E_SHAPE, -1, -1, -1)
+            arr = None
+        else:
+            exp = ir.validate(lengths, [[tuple(x) for x in st] for st in s])
+        ranges = np.array([x for st in s for x in st], dtype=np.int32).reshape(-1)
+        S = len(s) if all(len(st) == len(lengths) for st in s) else 0
+        if S == 0:
+            st = mt.mt_set_schedule(c.h, 0, ranges.ctypes.data_as(mt.I32P))
+        else:
+            st = mt.mt_set_schedule(c.h, S, ranges.ctypes.data_as(mt.I32P))
+        if exp[0] == ir.E_OK:
+            assert st == mt.MT_OK
+        else:
+            n_err += 1
+            assert st == mt.MT_ERR_VALIDATION
+            e = mt.mt_error_info()
+            mt.mt_last_error_info(c.h, C.byref(e))
+            assert (e.code, e.stage, e.tenant, e.op) == exp, (s, exp)
+    assert n_err > 1000
+
+
+def test_pointer_form_bit_exact():
+    lengths = (3, 2, 2)
+    c = host_ctx([_tiny_graph(L) for L in lengths])
+    for P in range(0, 4):
+        rows = [list(itertools.combinations_with_replacement(range(-1, L + 2), P)) for L in lengths]
+        rnd = random.Random(P)
+        for _ in range(400):
+            rho = [list(rnd.choice(r)) for r in rows]
+            rnd.shuffle(rho[0])
+            exp, ranges = ir.T(lengths, rho)
+            try:
+                c.set_schedule_pointers(rho)
+                got = (0, -1, -1, -1)
+            except mt.MTError as e:
+                assert e.status == mt.MT_ERR_VALIDATION
+                got = e.info
+            assert got == exp, (rho, got, exp)
+            if exp[0] == ir.E_OK:
+                assert c.get_schedule().tolist() == [[list(x) for x in st] for st in ranges]
+
+
+def test_paper_examples_through_abi():
+    lengths = (10, 4, 6)
+    c = host_ctx([_tiny_graph(L) for L in lengths])
+    c.set_schedule_pointers([[3, 5, 7], [1, 2, 3], [2, 2, 4]])
+    s = c.get_schedule()
+    assert s.shape[0] == 4
+    assert s[0].tolist() == [[0, 3], [0, 1], [0, 2]]      # Eq.4 stage 1
+    assert s[1].tolist() == [[3, 5], [1, 2], [2, 2]]      # Eq.5 stage 2, S3 None
+
+
+@pytest.mark.parametrize("config", ["c1", "c2", "c3", "c4", "c4b8"])
+def test_op_cost_and_sm_partition_match_oracle(config):
+    graphs = configs.tenants(config)
+    c = host_ctx(graphs)
+    for t, g in enumerate(graphs):
+        eb = 2 if g.precision == zoo.PREC_BF16 else 4
+        for j in range(g.n_ops):
+            assert c.op_cost(t, j) == ir.op_cost(g.nodes, j, g.batch, (g.in_c, g.in_h, g.in_w), eb)
+    L = [g.n_ops for g in graphs]
+    scheds = [configs.all_concurrent_pointers(L), configs.sequential_pointers(L),
+              configs.uniform_pointers(L)] + configs.sample_candidates(L, 40)[2:]
+    eb_of = lambda g: 2 if g.precision == zoo.PREC_BF16 else 4
+    for rho in scheds:
+        st, ranges = ir.T(L, rho)
+        if st[0] != ir.E_OK:
+            continue
+        c.set_schedule_pointers(rho)
+        got = c.sm_partition().tolist()
+        exp = [ir.sm_partition(w, 148) for w in ir.stage_weights(graphs, ranges, eb_of)]
+        assert got == exp
+
+
+def test_zoo_graphs_ingest_and_reject_bad_graphs():
+    for name, f in zoo.MODELS.items():
+        g = f()
+        c = host_ctx([g])
+        assert c.workspace_size() > 0
+    g = zoo.resnet18()
+    g.nodes[3] = dict(g.nodes[3], out_c=g.nodes[3]["out_c"] + 1)
+    with pytest.raises(mt.MTError):
+        host_ctx([g])
+    g = zoo.resnet18()
+    g.nodes[2] = dict(g.nodes[2], inputs=[5])          # not topological
+    with pytest.raises(mt.MTError):
+        host_ctx([g])
+
+
+def test_host_only_context_refuses_to_run():
+    c = host_ctx([zoo.tinyA()])
+    c.set_schedule_pointers([[]])
+    with pytest.raises(mt.MTError) as e:
+        c.run([0], [0])
+    assert e.value.status == mt.MT_ERR_STATE
