@@ -161,11 +161,11 @@ class GraphBuilder:
                     ceil_mode=int(ceil_mode))
         return self._add(node, (c, ho, wo), {})
 
-    def avgpool(self, x, k, s, p=0, count_include_pad=True):
+    def avgpool(self, x, k, s, p=0, count_include_pad=True, ceil_mode=False):
         c, h, w = self._shape(x)
-        ho, wo = _pool_out(h, k, s, p, False), _pool_out(w, k, s, p, False)
+        ho, wo = _pool_out(h, k, s, p, ceil_mode), _pool_out(w, k, s, p, ceil_mode)
         node = dict(kind=AVGPOOL, inputs=self._ids(x), kh=k, kw=k, sh=s, sw=s, ph=p, pw=p,
-                    count_include_pad=int(count_include_pad))
+                    count_include_pad=int(count_include_pad), ceil_mode=int(ceil_mode))
         return self._add(node, (c, ho, wo), {})
 
     def gap(self, x):
