@@ -211,6 +211,14 @@ mt_status mt_profile_batch_pointers(mt_ctx *ctx, int32_t n_cand, const int32_t *
 mt_status mt_get_activation(mt_ctx *ctx, int32_t tenant, int32_t op, void *host_dst,
                             size_t bytes);
 
+/* Debug tracing: when enabled, every executed tile appends one record of 8 uint64 to
+ * the caller's DEVICE buffer: [0] op | tile << 32 (global op id), [1] smid | cta << 32,
+ * [2] claim time, [3] dependencies satisfied, [4] tensor-core mainloop done (0 if none),
+ * [5] tile end, [6] home tenant of the CTA (-1 in baselines), [7] 0; times are %globaltimer ns.
+ * capacity = records; 0 / NULL disables.  Resets the record counter. */
+mt_status mt_set_trace(mt_ctx *ctx, void *dev_buf, int64_t capacity);
+mt_status mt_trace_count(mt_ctx *ctx, int64_t *n_records);
+
 mt_status mt_last_error_info(mt_ctx *ctx, mt_error_info *info);
 const char *mt_last_error(mt_ctx *ctx);
 /* static build/version string */

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstddef>
 #include <cstring>
 #include <map>
 #include <string>
@@ -32,6 +33,7 @@ struct mt_ctx {
   std::vector<WPack> wpacks;
   int64_t weight_bytes = 0, act_bytes = 0, partial_bytes = 0;
   int total_split_cnt = 0;
+  int total_blocks = 0;
   int sum_L = 0;
   Layout lay;
   char *ws = nullptr;
@@ -44,6 +46,8 @@ struct mt_ctx {
   // cached CUDA graphs of the graph baselines (keyed by mode; invalidated on pointer change)
   cudaGraphExec_t gexec[8] = {};
   const float *g_in[8][MT_MAXT] = {};
+  unsigned long long *trace = nullptr;
+  int64_t trace_cap = 0;
   float *g_out[8][MT_MAXT] = {};
 };
 
@@ -318,17 +322,15 @@ static mt_status plan_graphs(mt_ctx *c) {
       }
       // dependencies: every producer op this op reads (global ids)
       d.n_dep = 0;
+      auto add_dep = [&](int gid_dep, int kind) {
+        for (int r = 0; r < d.n_dep; ++r)
+          if (d.deps[r] == gid_dep) { d.dep_kind[r] |= kind; return; }
+        d.deps[d.n_dep] = gid_dep;
+        d.dep_kind[d.n_dep++] = kind;
+      };
       for (int q = 0; q < n.n_inputs; ++q)
-        if (n.inputs[q] >= 0) {
-          bool dup = false;
-          for (int r = 0; r < d.n_dep; ++r) dup |= d.deps[r] == tn.op_base + n.inputs[q];
-          if (!dup) d.deps[d.n_dep++] = tn.op_base + n.inputs[q];
-        }
-      if (n.kind == MT_CONV && n.residual >= 0) {
-        bool dup = false;
-        for (int r = 0; r < d.n_dep; ++r) dup |= d.deps[r] == tn.op_base + n.residual;
-        if (!dup) d.deps[d.n_dep++] = tn.op_base + n.residual;
-      }
+        if (n.inputs[q] >= 0) add_dep(tn.op_base + n.inputs[q], 1);
+      if (n.kind == MT_CONV && n.residual >= 0) add_dep(tn.op_base + n.residual, 2);
       h.scale = n.scale;
       h.shift = n.shift;
       // --- algorithmic cost (SURVEY d.4 B_op), identical to oracle/ir.py op_cost ---
@@ -363,7 +365,16 @@ static mt_status plan_graphs(mt_ctx *c) {
         case MT_CONV:
           if (n.groups > 1) {
             d.tk = TK_DW;
-            d.tiles = (int)cdiv((int64_t)g.batch * os.h * os.w * (os.c / 8), MT_NTHREADS * MT_EW_PER_THREAD);
+            if (n.kh == 3 && n.kw == 3 && n.sh == n.sw && (n.sh == 1 || n.sh == 2)) {
+              // whole output rows per tile (row-run kernel): ~MT_NTHREADS*1.5 items per tile
+              const int run = n.sh == 1 ? 4 : 2;
+              const int64_t per_row = cdiv(os.w, run) * (os.c / 8);
+              const int rows = (int)std::max<int64_t>(1, (MT_NTHREADS * 3 / 2) / per_row);
+              d.pix_tile = rows * os.w;
+            } else {
+              d.pix_tile = (int)std::max<int64_t>(1, (MT_NTHREADS * MT_EW_PER_THREAD) / (os.c / 8));
+            }
+            d.tiles = (int)cdiv((int64_t)g.batch * os.h * os.w, d.pix_tile);
             wp.mode = 3;
             wp.bytes = (int64_t)n.kh * n.kw * os.c * eb;
           } else if (bf16) {
@@ -377,8 +388,8 @@ static mt_status plan_graphs(mt_ctx *c) {
             d.tiles_n = (int)cdiv(os.c, d.bn);
             const int tmn = d.tiles_m * d.tiles_n;
             int splits = 1;
-            if (tmn < 74 && d.nkb >= 4) {
-              splits = (int)std::min<int64_t>(std::min<int64_t>(cdiv(148, tmn), d.nkb / 2), 16);
+            if (tmn < 74 && d.nkb >= 8) {
+              splits = (int)std::min<int64_t>(std::min<int64_t>(cdiv(148, tmn), d.nkb / 4), 16);
               splits = std::max(splits, 1);
             }
             d.kb_per_split = (int)cdiv(d.nkb, splits);
@@ -408,11 +419,12 @@ static mt_status plan_graphs(mt_ctx *c) {
         case MT_MAXPOOL:
         case MT_AVGPOOL:
           d.tk = TK_POOL;
-          d.tiles = (int)cdiv((int64_t)g.batch * os.h * os.w * (os.c / 8), MT_NTHREADS * MT_EW_PER_THREAD);
+          d.pix_tile = (int)std::max<int64_t>(1, (MT_NTHREADS * MT_EW_PER_THREAD) / (os.c / 8));
+          d.tiles = (int)cdiv((int64_t)g.batch * os.h * os.w, d.pix_tile);
           break;
         case MT_GLOBAL_AVGPOOL:
           d.tk = TK_GAP;
-          d.tiles = (int)cdiv((int64_t)g.batch * (os.c / 8), MT_NTHREADS);
+          d.tiles = (int)(g.batch * cdiv(os.c / 8, 32));
           break;
         case MT_FC:
           d.tk = TK_FC;
@@ -425,7 +437,8 @@ static mt_status plan_graphs(mt_ctx *c) {
           break;
         default:
           d.tk = TK_ELT;
-          d.tiles = (int)cdiv((int64_t)g.batch * os.h * os.w * (os.c / 8), MT_NTHREADS * MT_EW_PER_THREAD);
+          d.pix_tile = (int)std::max<int64_t>(1, (MT_NTHREADS * MT_EW_PER_THREAD) / (os.c / 8));
+          d.tiles = (int)cdiv((int64_t)g.batch * os.h * os.w, d.pix_tile);
           break;
       }
       (void)cin_real;
@@ -438,8 +451,22 @@ static mt_status plan_graphs(mt_ctx *c) {
       if (d.tiles < 1) d.tiles = 1;
     }
   }
-  for (auto &h : c->ops)
-    for (int q = 0; q < h.d.n_dep; ++q) h.d.dep_tiles[q] = c->ops[h.d.deps[q]].d.tiles;
+  int64_t nblk_total = 0;
+  for (auto &h : c->ops) {
+    OpDesc &d = h.d;
+    const int64_t npix = (int64_t)d.N * d.Ho * d.Wo;
+    switch (d.tk) {
+      case TK_CONV_TC: d.pix_blk = MT_BM; d.blk_need = d.tiles_n; break;
+      case TK_CONV_SIMT: d.pix_blk = MT_SIMT_BM; d.blk_need = d.tiles_n; break;
+      case TK_GAP: d.pix_blk = 1; d.blk_need = (int)cdiv(d.Co / 8, 32); break;
+      case TK_FC: d.pix_blk = MT_FC_BATCH; d.blk_need = (int)cdiv(d.Co, MT_FC_ROWS); break;
+      default: d.pix_blk = d.pix_tile; d.blk_need = 1; break;
+    }
+    d.nblk = (int)cdiv(npix, d.pix_blk);
+    d.blk_off = (int)nblk_total;
+    nblk_total += d.nblk;
+  }
+  c->total_blocks = (int)nblk_total;
   c->weight_bytes = wbytes;
   c->partial_bytes = pbytes;
   c->total_split_cnt = split_cnt;
@@ -456,6 +483,7 @@ static mt_status plan_graphs(mt_ctx *c) {
   L.ctl = take(sizeof(CtlBlock));
   L.claim = take(sizeof(int32_t) * total);
   L.done = take(sizeof(int32_t) * total);
+  L.blk = take(sizeof(int32_t) * std::max(c->total_blocks, 1));
   L.splitcnt = take(sizeof(int32_t) * std::max(split_cnt, 1));
   L.counters_bytes = off;
   L.ops = take(sizeof(OpDesc) * total);
@@ -566,6 +594,8 @@ static RunArgs base_args(mt_ctx *c, const float *const *inputs, float *const *ou
   a.steal = c->steal;
   a.claim = (int32_t *)(c->ws + c->lay.claim);
   a.done = (int32_t *)(c->ws + c->lay.done);
+  a.blkcnt = (int32_t *)(c->ws + c->lay.blk);
+  a.n_blk = c->total_blocks;
   a.splitcnt = (int32_t *)(c->ws + c->lay.splitcnt);
   a.ctl = (CtlBlock *)(c->ws + c->lay.ctl);
   a.ts = (unsigned long long *)(c->ws + c->lay.run_ts);
@@ -573,6 +603,8 @@ static RunArgs base_args(mt_ctx *c, const float *const *inputs, float *const *ou
   a.timeout_ns = (unsigned long long)c->timeout_ms * 1000000ull;
   a.n_ops = (int)c->ops.size();
   a.n_pack = 0;
+  a.trace = c->trace;
+  a.trace_cap = (int32_t)c->trace_cap;
   for (int t = 0; t < N; ++t) {
     const mt_graph &g = c->T[t].g;
     a.inputs[t] = inputs ? inputs[t] : nullptr;
@@ -1173,6 +1205,26 @@ mt_status mt_get_activation(mt_ctx *c, int32_t t, int32_t op, void *host, size_t
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy2D(host, (size_t)h.d.Co * eb, src, (size_t)h.out.cs * eb, (size_t)h.d.Co * eb, rows,
                   cudaMemcpyDeviceToHost));
+  return MT_OK;
+}
+
+mt_status mt_set_trace(mt_ctx *c, void *dev, int64_t capacity) {
+  mt_status st = check_ready(c, false);
+  if (st != MT_OK) return st;
+  if (capacity < 0 || capacity > (1 << 30) || (capacity > 0 && !dev)) return fail(c, MT_ERR_ARG, "bad trace buffer");
+  c->trace = capacity > 0 ? (unsigned long long *)dev : nullptr;
+  c->trace_cap = capacity;
+  CK(cudaMemset(c->ws + c->lay.ctl + offsetof(CtlBlock, trace_count), 0, sizeof(unsigned)));
+  return MT_OK;
+}
+
+mt_status mt_trace_count(mt_ctx *c, int64_t *n) {
+  mt_status st = check_ready(c, false);
+  if (st != MT_OK) return st;
+  if (!n) return fail(c, MT_ERR_ARG, "null");
+  unsigned v = 0;
+  CK(cudaMemcpy(&v, c->ws + c->lay.ctl + offsetof(CtlBlock, trace_count), sizeof v, cudaMemcpyDeviceToHost));
+  *n = v;
   return MT_OK;
 }
 

@@ -34,11 +34,14 @@ struct CtaShared {
   unsigned long long bar_empty[MT_STAGES];
   unsigned long long bar_accf;
   uint32_t tmem_base;
-  int op, tile, last, ok, home;
+  int op, tile, last, ok, home, ten;
+  unsigned long long t_pick, t_deps, t_mma, t_run;
   int cur[MT_MAXT], end[MT_MAXT];
+  uint32_t complete[64];      // bitset of ops observed fully complete (global op id < 2048)
+  float esc[128], esh[128];   // epilogue scale / shift of the current conv tile's columns
   OpDesc d;
 };
-static constexpr int SMEM_BYTES = 1024 + PIPE_BYTES + ((sizeof(CtaShared) + 127) / 128) * 128;
+static constexpr int SMEM_BYTES = 1024 + PIPE_BYTES;   // + static __shared__ CtaShared
 
 struct PipeState {
   uint32_t fill;       // k-blocks loaded so far by this CTA (stage ring position)
@@ -68,6 +71,12 @@ __device__ __forceinline__ unsigned ld_acquire_u(const unsigned *p) {
 }
 __device__ __forceinline__ void st_release_u(unsigned *p, unsigned v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_add(int *p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
@@ -169,6 +178,42 @@ __device__ __forceinline__ void ld8_cg(const float *p, float *v) {
   asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w) : "l"(p + 4));
   v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
 }
+// raw (unconverted) 8-channel vectors: 4 registers for bf16, 8 for fp32
+template <typename T> struct Raw8;
+template <> struct Raw8<bf16> { uint4 u; };
+template <> struct Raw8<float> { float4 a, b; };
+__device__ __forceinline__ void ldraw_cg(const bf16 *p, Raw8<bf16> &r) {
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.u.x), "=r"(r.u.y), "=r"(r.u.z), "=r"(r.u.w) : "l"(p));
+}
+__device__ __forceinline__ void ldraw_cg(const float *p, Raw8<float> &r) {
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w) : "l"(p));
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.b.x), "=f"(r.b.y), "=f"(r.b.z), "=f"(r.b.w) : "l"(p + 4));
+}
+__device__ __forceinline__ Raw8<bf16> ldraw_nc(const bf16 *p) {
+  Raw8<bf16> r;
+  r.u = __ldg(reinterpret_cast<const uint4 *>(p));
+  return r;
+}
+__device__ __forceinline__ Raw8<float> ldraw_nc(const float *p) {
+  Raw8<float> r;
+  r.a = __ldg(reinterpret_cast<const float4 *>(p));
+  r.b = __ldg(reinterpret_cast<const float4 *>(p + 4));
+  return r;
+}
+__device__ __forceinline__ void zero_raw(Raw8<bf16> &r) { r.u = make_uint4(0, 0, 0, 0); }
+__device__ __forceinline__ void zero_raw(Raw8<float> &r) { r.a = r.b = make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ void cvt8(const Raw8<bf16> &r, float *v) {
+  const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&r.u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void cvt8(const Raw8<float> &r, float *v) {
+  v[0] = r.a.x; v[1] = r.a.y; v[2] = r.a.z; v[3] = r.a.w; v[4] = r.b.x; v[5] = r.b.y; v[6] = r.b.z; v[7] = r.b.w;
+}
 __device__ __forceinline__ void ld8_nc(const bf16 *p, float *v) {  // immutable weights
   uint4 u = __ldg(reinterpret_cast<const uint4 *>(p));
   const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
@@ -239,11 +284,10 @@ __device__ __forceinline__ void store_out8(const RunArgs &a, const OpDesc &d, in
 // Deterministic split-K: fp32 partials in workspace, the last-arriving CTA sums them in split
 // order 0..S-1 and runs the epilogue.
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ void conv_epilogue_vals(const RunArgs &a, const OpDesc &d, int m, int n,
-                                                   float *v) {
+__device__ __forceinline__ void conv_epilogue_vals(const RunArgs &a, const OpDesc &d, const CtaShared &sh,
+                                                   int m, int n0, int col, float *v) {
+  const int n = n0 + col;
   const int nvalid = min(8, d.Co - n);
-  const float *sc = reinterpret_cast<const float *>(d.scale);
-  const float *sh = reinterpret_cast<const float *>(d.shift);
   float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (d.flags & OPF_RES) {
     const bf16 *rp = reinterpret_cast<const bf16 *>(d.res) + (int64_t)m * d.res_cs + d.res_co + n;
@@ -252,22 +296,68 @@ __device__ __forceinline__ void conv_epilogue_vals(const RunArgs &a, const OpDes
       for (int e = 0; e < nvalid; ++e) r[e] = ld1_cg(rp + e);
   }
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    if (e < nvalid) v[e] = act_f(fmaf(v[e], __ldg(sc + n + e), __ldg(sh + n + e)) + r[e], d.act);
-  }
+  for (int e = 0; e < 8; ++e) v[e] = act_f(fmaf(v[e], sh.esc[col + e], sh.esh[col + e]) + r[e], d.act);
   store_out8<bf16>(a, d, m, n, v, nvalid);
+}
+
+struct ConvTile {
+  int tmn, ks, m0, n0, kb0, nk;
+};
+__device__ __forceinline__ ConvTile conv_tile_coords(const OpDesc &d, int tile) {
+  ConvTile c;
+  const int S = d.splits;
+  c.tmn = tile / S;
+  c.ks = tile - c.tmn * S;
+  const int mt = c.tmn / d.tiles_n, nt = c.tmn - (c.tmn / d.tiles_n) * d.tiles_n;
+  c.m0 = mt * MT_BM;
+  c.n0 = nt * d.bn;
+  c.kb0 = c.ks * d.kb_per_split;
+  c.nk = min(d.nkb, c.kb0 + d.kb_per_split) - c.kb0;
+  return c;
+}
+
+// Issue the weight (B) tiles of the first min(nk, MT_STAGES) k-blocks and stage the epilogue
+// constants.  Needs no producer data, so the executor runs it BEFORE waiting for the tile's
+// dependencies: the weight stream overlaps the wait.  Each k-block is its own commit group.
+__device__ void conv_tc_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaShared &sh,
+                                 const PipeState &ps) {
+  const int tid = threadIdx.x;
+  const ConvTile ct = conv_tile_coords(d, tile);
+  const bf16 *Wt = reinterpret_cast<const bf16 *>(d.w);
+  const uint32_t sB = smem_u32(smem) + MT_STAGES * A_STAGE;
+  const uint32_t bar_empty0 = smem_u32(&sh.bar_empty[0]);
+  const int c = tid & 7;
+  for (int i = 0; i < MT_STAGES; ++i) {
+    if (i < ct.nk) {
+      const uint32_t f = ps.fill + i;
+      const int s = f % MT_STAGES;
+      if (f >= MT_STAGES) mbar_wait(bar_empty0 + 8 * s, ((f / MT_STAGES) - 1) & 1);
+      const int kb = ct.kb0 + i;
+      const uint32_t sb = sB + s * B_STAGE;
+      for (int row = tid >> 3; row < d.bn; row += 32) {
+        const bf16 *src = Wt + (int64_t)(ct.n0 + row) * d.Kpad + kb * MT_BK + c * 8;
+        cp_async16(sb + row * 128 + ((c ^ (row & 7)) << 4), src, true);
+      }
+    }
+    cp_async_commit();
+  }
+  if (tid < d.bn) {
+    const int n = ct.n0 + tid;
+    sh.esc[tid] = n < d.Co ? __ldg(reinterpret_cast<const float *>(d.scale) + n) : 0.f;
+    sh.esh[tid] = n < d.Co ? __ldg(reinterpret_cast<const float *>(d.shift) + n) : 0.f;
+  }
+  // the rest of this split's weight rows -> L2 (one bulk prefetch per row)
+  if (ct.nk > MT_STAGES && tid < d.bn)
+    prefetch_l2_bulk(Wt + (int64_t)(ct.n0 + tid) * d.Kpad + (ct.kb0 + MT_STAGES) * MT_BK,
+                     (uint32_t)(ct.nk - MT_STAGES) * MT_BK * 2);
 }
 
 __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_t *smem,
                              CtaShared &sh, PipeState &ps) {
   const int tid = threadIdx.x;
   const int S = d.splits;
-  const int tmn = tile / S, ks = tile - tmn * S;
-  const int mt = tmn % d.tiles_m, nt = tmn / d.tiles_m;
-  const int m0 = mt * MT_BM, n0 = nt * d.bn;
-  const int kb0 = ks * d.kb_per_split;
-  const int kb1 = min(d.nkb, kb0 + d.kb_per_split);
-  const int nk = kb1 - kb0;
+  const ConvTile ct = conv_tile_coords(d, tile);
+  const int tmn = ct.tmn, ks = ct.ks, m0 = ct.m0, n0 = ct.n0, kb0 = ct.kb0, nk = ct.nk;
   const bf16 *X = in_ptr<bf16>(a, d);
   const bf16 *Wt = reinterpret_cast<const bf16 *>(d.w);
   const int HoWo = d.Ho * d.Wo;
@@ -292,11 +382,14 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
   const uint32_t bar_empty0 = smem_u32(&sh.bar_empty[0]);
   const uint32_t bar_accf = smem_u32(&sh.bar_accf);
 
+  // commit groups: MT_STAGES B-prefetch groups (conv_tc_prefetch) precede the loop's groups;
+  // group NS + j holds A (and, for j >= NS, B) of k-block j, so wait_group<NS-1> at iteration
+  // i = j + NS - 1 completes both the prefetched B of k-block j and its A.
   for (int i = 0; i < nk + MT_STAGES - 1; ++i) {
     if (i < nk) {
       const uint32_t f = ps.fill + i;
       const int s = f % MT_STAGES;
-      if (f >= MT_STAGES) mbar_wait(bar_empty0 + 8 * s, ((f / MT_STAGES) - 1) & 1);
+      if (i >= MT_STAGES) mbar_wait(bar_empty0 + 8 * s, ((f / MT_STAGES) - 1) & 1);
       const int kb = kb0 + i;
       const int k = kb * MT_BK + c * 8;
       const bool kv = k < d.K;
@@ -312,10 +405,12 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
         const bf16 *src = valid ? X + (int64_t)(pbase[i2] + hi * d.W + wi) * d.in_cs + d.in_co + ci : X;
         cp_async16(sa + row * 128 + ((c ^ (row & 7)) << 4), src, valid);
       }
-      const uint32_t sb = sB + s * B_STAGE;
-      for (int row = tid >> 3; row < d.bn; row += 32) {
-        const bf16 *src = Wt + (int64_t)(n0 + row) * d.Kpad + kb * MT_BK + c * 8;
-        cp_async16(sb + row * 128 + ((c ^ (row & 7)) << 4), src, true);
+      if (i >= MT_STAGES) {
+        const uint32_t sb = sB + s * B_STAGE;
+        for (int row = tid >> 3; row < d.bn; row += 32) {
+          const bf16 *src = Wt + (int64_t)(n0 + row) * d.Kpad + kb * MT_BK + c * 8;
+          cp_async16(sb + row * 128 + ((c ^ (row & 7)) << 4), src, true);
+        }
       }
     }
     cp_async_commit();
@@ -337,10 +432,12 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
       }
     }
   }
+  cp_async_wait<0>();
   ps.fill += nk;
   mbar_wait(bar_accf, ps.acc_phase);
   ps.acc_phase ^= 1;
   tc_fence_after();
+  if (tid == 0) sh.t_mma = gtimer();
 
   // epilogue: warp w drains TMEM lanes 32*(w&3).. and column half (w>>2)
   const int warp = tid >> 5, lane = tid & 31;
@@ -353,7 +450,7 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
     for (int col = half * hcols; col < (half + 1) * hcols; col += 8) {
       float v[8];
       tmem_ld8(tl + col, v);
-      if (m < d.M && n0 + col < d.Co) conv_epilogue_vals(a, d, m, n0 + col, v);
+      if (m < d.M && n0 + col < d.Co) conv_epilogue_vals(a, d, sh, m, n0, col, v);
     }
   } else {
     float *ws = reinterpret_cast<float *>(d.ws);
@@ -361,8 +458,9 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
       float v[8];
       tmem_ld8(tl + col, v);
       float *p = ws + ((int64_t)(tmn * S + ks) * d.bn + col) * MT_BM + r;
+      if (m < d.M && n0 + col < d.Co)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) __stcg(p + e * MT_BM, v[e]);
+        for (int e = 0; e < 8; ++e) __stcg(p + e * MT_BM, v[e]);
     }
     tc_fence_before();
     __syncthreads();
@@ -376,15 +474,15 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
       }
     }
     __syncthreads();
-    if (sh.last) {
-      for (int col = half * hcols; col < (half + 1) * hcols; col += 8) {
+    if (sh.last && m < d.M) {   // only rows that exist are reduced (M may be << 128 at b=1)
+      for (int col = half * hcols; col < (half + 1) * hcols && n0 + col < d.Co; col += 8) {
         float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (int s2 = 0; s2 < S; ++s2) {  // fixed summation order: deterministic
           const float *p = ws + ((int64_t)(tmn * S + s2) * d.bn + col) * MT_BM + r;
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[e] += __ldcg(p + e * MT_BM);
         }
-        if (m < d.M && n0 + col < d.Co) conv_epilogue_vals(a, d, m, n0 + col, v);
+        if (m < d.M && n0 + col < d.Co) conv_epilogue_vals(a, d, sh, m, n0, col, v);
       }
     }
   }
@@ -400,7 +498,7 @@ __device__ void conv_simt_tile(const RunArgs &a, const OpDesc &d, int tile, uint
   float *As = reinterpret_cast<float *>(smem);                 // [BK][BM]
   float *Bs = As + MT_SIMT_BK * MT_SIMT_BM;                    // [BK][BN]
   const int tid = threadIdx.x;
-  const int mt = tile % d.tiles_m, nt = tile / d.tiles_m;
+  const int mt = tile / d.tiles_n, nt = tile - (tile / d.tiles_n) * d.tiles_n;
   const int m0 = mt * MT_SIMT_BM, n0 = nt * MT_SIMT_BN;
   const T *X = in_ptr<T>(a, d);
   const float *Wt = reinterpret_cast<const float *>(d.w);
@@ -468,69 +566,182 @@ __device__ void conv_simt_tile(const RunArgs &a, const OpDesc &d, int tile, uint
 // ------------------------------------------------------------------------------------------
 // a6: depthwise conv (+ folded BN + act); item = (output pixel, 8-channel group)
 // ------------------------------------------------------------------------------------------
-template <typename T>
-__device__ void dw_tile(const RunArgs &a, const OpDesc &d, int tile) {
-  const T *X = in_ptr<T>(a, d);
-  const T *Wt = reinterpret_cast<const T *>(d.w);
-  const int cg = d.C >> 3;
-  const int64_t items = (int64_t)d.N * d.Ho * d.Wo * cg;
-  const float *sc = reinterpret_cast<const float *>(d.scale);
-  const float *sf = reinterpret_cast<const float *>(d.shift);
+template <typename T, int KH, int KW>
+__device__ __forceinline__ void dw_item(const RunArgs &a, const OpDesc &d, const T *X, const T *Wt,
+                                        int64_t pix, int g) {
+  const int n = (int)(pix / (d.Ho * d.Wo));
+  const int rem = (int)(pix - (int64_t)n * d.Ho * d.Wo);
+  const int ho = rem / d.Wo, wo = rem - ho * d.Wo;
+  const int kh = KH > 0 ? KH : d.kh, kw = KW > 0 ? KW : d.kw;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  constexpr int NT = (KH > 0 && KW > 0) ? KH * KW : 1;
+  if constexpr (NT > 1) {
+    Raw8<T> xr[NT];
+    // issue every tap's load first (memory-level parallelism), out-of-window taps read zeros
 #pragma unroll
-  for (int e = 0; e < MT_EW_PER_THREAD; ++e) {
-    const int64_t it = (int64_t)tile * (MT_NTHREADS * MT_EW_PER_THREAD) + e * MT_NTHREADS + threadIdx.x;
-    if (it >= items) break;
-    const int64_t pix = it / cg;
-    const int g = (int)(it - pix * cg);
-    const int n = (int)(pix / (d.Ho * d.Wo));
-    const int rem = (int)(pix - (int64_t)n * d.Ho * d.Wo);
-    const int ho = rem / d.Wo, wo = rem - ho * d.Wo;
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int r = 0; r < d.kh; ++r) {
+    for (int t = 0; t < NT; ++t) {
+      const int hi = ho * d.sh - d.ph + t / KW, wi = wo * d.sw - d.pw + t % KW;
+      if (hi >= 0 && hi < d.H && wi >= 0 && wi < d.W)
+        ldraw_cg(X + ((int64_t)(n * d.H + hi) * d.W + wi) * d.in_cs + d.in_co + g * 8, xr[t]);
+      else
+        zero_raw(xr[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      float w[8], x[8];
+      ld8_nc(Wt + (int64_t)t * d.C + g * 8, w);
+      cvt8(xr[t], x);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = fmaf(x[q], w[q], acc[q]);
+    }
+  } else {
+    for (int r = 0; r < kh; ++r) {
       const int hi = ho * d.sh - d.ph + r;
       if (hi < 0 || hi >= d.H) continue;
-      for (int s = 0; s < d.kw; ++s) {
+      for (int s = 0; s < kw; ++s) {
         const int wi = wo * d.sw - d.pw + s;
         if (wi < 0 || wi >= d.W) continue;
         float x[8], w[8];
         ld8_cg(X + ((int64_t)(n * d.H + hi) * d.W + wi) * d.in_cs + d.in_co + g * 8, x);
-        ld8_nc(Wt + (int64_t)(r * d.kw + s) * d.C + g * 8, w);
+        ld8_nc(Wt + (int64_t)(r * kw + s) * d.C + g * 8, w);
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc[q] = fmaf(x[q], w[q], acc[q]);
       }
     }
+  }
+  const float *sc = reinterpret_cast<const float *>(d.scale);
+  const float *sf = reinterpret_cast<const float *>(d.shift);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = act_f(fmaf(acc[q], __ldg(sc + g * 8 + q), __ldg(sf + g * 8 + q)), d.act);
-    store_out8<T>(a, d, pix, g * 8, acc, 8);
+  for (int q = 0; q < 8; ++q) acc[q] = act_f(fmaf(acc[q], __ldg(sc + g * 8 + q), __ldg(sf + g * 8 + q)), d.act);
+  store_out8<T>(a, d, pix, g * 8, acc, 8);
+}
+
+// 3x3 depthwise, row-run form: one thread computes RUN consecutive output pixels of one row for
+// one 8-channel group, so the (RUN-1)*S+3 input columns of each kernel row are loaded once and
+// reused by neighbouring outputs; all loads are issued before the arithmetic.  A tile = whole
+// output rows (pix_tile = rows * Wo), item = (row, run segment, channel group), group fastest.
+template <typename T, int S, int RUN>
+__device__ void dw3_tile(const RunArgs &a, const OpDesc &d, int tile) {
+  constexpr int NC = (RUN - 1) * S + 3;
+  const T *X = in_ptr<T>(a, d);
+  const T *Wt = reinterpret_cast<const T *>(d.w);
+  const float *sc = reinterpret_cast<const float *>(d.scale);
+  const float *sf = reinterpret_cast<const float *>(d.shift);
+  const int cg = d.C >> 3;
+  const int nseg = (d.Wo + RUN - 1) / RUN;
+  const int rows = d.pix_tile / d.Wo;
+  const int row0 = tile * rows;
+  const int nrows = min(rows, d.N * d.Ho - row0);
+  const int items = nrows * nseg * cg;
+  const int H = d.H, W = d.W, cs = d.in_cs;
+  for (int it = threadIdx.x; it < items; it += MT_NTHREADS) {
+    const int g = it % cg;
+    const int rs = it / cg;
+    const int seg = rs % nseg;
+    const int gr = row0 + rs / nseg;            // global output row (n*Ho + ho)
+    const int n = gr / d.Ho, ho = gr - n * d.Ho;
+    const int wo0 = seg * RUN;
+    const int wi0 = wo0 * S - d.pw;
+    const T *xb = X + (int64_t)n * H * W * cs + d.in_co + g * 8;
+    Raw8<T> xr[3][NC];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int hi = ho * S - d.ph + r;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int wi = wi0 + c;
+        if (hi >= 0 && hi < H && wi >= 0 && wi < W) ldraw_cg(xb + (int64_t)(hi * W + wi) * cs, xr[r][c]);
+        else zero_raw(xr[r][c]);
+      }
+    }
+    float acc[RUN][8];
+#pragma unroll
+    for (int o = 0; o < RUN; ++o)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[o][q] = 0.f;
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int s2 = 0; s2 < 3; ++s2) {
+        float w[8];
+        ld8_nc(Wt + (r * 3 + s2) * d.C + g * 8, w);
+#pragma unroll
+        for (int o = 0; o < RUN; ++o) {
+          float x[8];
+          cvt8(xr[r][o * S + s2], x);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[o][q] = fmaf(x[q], w[q], acc[o][q]);
+        }
+      }
+    float scv[8], sfv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { scv[q] = __ldg(sc + g * 8 + q); sfv[q] = __ldg(sf + g * 8 + q); }
+#pragma unroll
+    for (int o = 0; o < RUN; ++o) {
+      if (wo0 + o < d.Wo) {
+        float y[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) y[q] = act_f(fmaf(acc[o][q], scv[q], sfv[q]), d.act);
+        store_out8<T>(a, d, (int64_t)gr * d.Wo + wo0 + o, g * 8, y, 8);
+      }
+    }
+  }
+}
+
+template <typename T>
+__device__ void dw_tile(const RunArgs &a, const OpDesc &d, int tile) {
+  if (d.kh == 3 && d.kw == 3 && d.sh == d.sw && (d.sh == 1 || d.sh == 2) && d.pix_tile % d.Wo == 0) {
+    if (d.sh == 1) dw3_tile<T, 1, 4>(a, d, tile);
+    else dw3_tile<T, 2, 2>(a, d, tile);
+    return;
+  }
+  const T *X = in_ptr<T>(a, d);
+  const T *Wt = reinterpret_cast<const T *>(d.w);
+  const int cg = d.C >> 3;
+  const int p0 = tile * d.pix_tile;
+  const int np = min(d.pix_tile, d.N * d.Ho * d.Wo - p0);
+  for (int it = threadIdx.x; it < np * cg; it += MT_NTHREADS) {
+    const int pix = p0 + it / cg;
+    const int g = it % cg;
+    dw_item<T, 0, 0>(a, d, X, Wt, pix, g);
   }
 }
 
 // ------------------------------------------------------------------------------------------
 // a7: max / avg pooling (PyTorch window semantics: padding, ceil_mode, count_include_pad)
 // ------------------------------------------------------------------------------------------
-template <typename T>
-__device__ void pool_tile(const RunArgs &a, const OpDesc &d, int tile) {
-  const T *X = in_ptr<T>(a, d);
-  const int cg = d.C >> 3;
-  const int64_t items = (int64_t)d.N * d.Ho * d.Wo * cg;
+template <typename T, int K>
+__device__ __forceinline__ void pool_item(const RunArgs &a, const OpDesc &d, const T *X, int64_t pix, int g) {
   const bool is_max = d.kind == 4;
+  const int n = (int)(pix / (d.Ho * d.Wo));
+  const int rem = (int)(pix - (int64_t)n * d.Ho * d.Wo);
+  const int ho = rem / d.Wo, wo = rem - ho * d.Wo;
+  const int hs = ho * d.sh - d.ph, ws = wo * d.sw - d.pw;
+  const int he = min(hs + d.kh, d.H + d.ph), we = min(ws + d.kw, d.W + d.pw);
+  int div = (he - hs) * (we - ws);
+  const int h0 = max(hs, 0), h1 = min(he, d.H), w0 = max(ws, 0), w1 = min(we, d.W);
+  if (!d.cip) div = (h1 - h0) * (w1 - w0);
+  float acc[8];
 #pragma unroll
-  for (int e = 0; e < MT_EW_PER_THREAD; ++e) {
-    const int64_t it = (int64_t)tile * (MT_NTHREADS * MT_EW_PER_THREAD) + e * MT_NTHREADS + threadIdx.x;
-    if (it >= items) break;
-    const int64_t pix = it / cg;
-    const int g = (int)(it - pix * cg);
-    const int n = (int)(pix / (d.Ho * d.Wo));
-    const int rem = (int)(pix - (int64_t)n * d.Ho * d.Wo);
-    const int ho = rem / d.Wo, wo = rem - ho * d.Wo;
-    const int hs = ho * d.sh - d.ph, ws = wo * d.sw - d.pw;
-    const int he = min(hs + d.kh, d.H + d.ph), we = min(ws + d.kw, d.W + d.pw);
-    int div = (he - hs) * (we - ws);
-    const int h0 = max(hs, 0), h1 = min(he, d.H), w0 = max(ws, 0), w1 = min(we, d.W);
-    if (!d.cip) div = (h1 - h0) * (w1 - w0);
-    float acc[8];
+  for (int q = 0; q < 8; ++q) acc[q] = is_max ? -INFINITY : 0.f;
+  if constexpr (K > 0) {
+    Raw8<T> xr[K * K];
+    bool v[K * K];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = is_max ? -INFINITY : 0.f;
+    for (int t = 0; t < K * K; ++t) {
+      const int hi = h0 + t / K, wi = w0 + t % K;
+      v[t] = hi < h1 && wi < w1;
+      if (v[t]) ldraw_cg(X + ((int64_t)(n * d.H + hi) * d.W + wi) * d.in_cs + d.in_co + g * 8, xr[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < K * K; ++t)
+      if (v[t]) {
+        float x[8];
+        cvt8(xr[t], x);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = is_max ? fmaxf(acc[q], x[q]) : acc[q] + x[q];
+      }
+  } else {
     for (int hi = h0; hi < h1; ++hi)
       for (int wi = w0; wi < w1; ++wi) {
         float x[8];
@@ -538,42 +749,122 @@ __device__ void pool_tile(const RunArgs &a, const OpDesc &d, int tile) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc[q] = is_max ? fmaxf(acc[q], x[q]) : acc[q] + x[q];
       }
-    if (!is_max) {
-      const float inv = 1.f / (float)div;
+  }
+  if (!is_max) {
+    const float inv = 1.f / (float)div;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = acc[q] * inv;
-    }
-    store_out8<T>(a, d, pix, g * 8, acc, 8);
+    for (int q = 0; q < 8; ++q) acc[q] = acc[q] * inv;
+  }
+  store_out8<T>(a, d, pix, g * 8, acc, 8);
+}
+
+template <typename T>
+__device__ void pool_tile(const RunArgs &a, const OpDesc &d, int tile) {
+  const T *X = in_ptr<T>(a, d);
+  const int cg = d.C >> 3;
+  const int64_t p0 = (int64_t)tile * d.pix_tile;
+  const int64_t np = min((int64_t)d.pix_tile, (int64_t)d.N * d.Ho * d.Wo - p0);
+  for (int it = threadIdx.x; it < np * cg; it += MT_NTHREADS) {
+    const int64_t pix = p0 + it / cg;
+    const int g = it - (it / cg) * cg;
+    if (d.kh <= 2 && d.kw <= 2) pool_item<T, 2>(a, d, X, pix, g);
+    else if (d.kh <= 3 && d.kw <= 3) pool_item<T, 3>(a, d, X, pix, g);
+    else pool_item<T, 0>(a, d, X, pix, g);
   }
 }
 
-// global average pool; item = (n, 8-channel group)
+// global average pool: tile = (n, 32 channel groups); thread = (group, pixel lane of 8); each
+// lane sums pixels p = lane, lane+8, ... then lanes are combined in a fixed tree (deterministic)
 template <typename T>
-__device__ void gap_tile(const RunArgs &a, const OpDesc &d, int tile) {
+__device__ void gap_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_t *smem) {
   const T *X = in_ptr<T>(a, d);
   const int cg = d.C >> 3;
-  const int64_t it = (int64_t)tile * MT_NTHREADS + threadIdx.x;
-  if (it >= (int64_t)d.N * cg) return;
-  const int n = (int)(it / cg), g = (int)(it - (int64_t)n * cg);
+  const int tiles_c = (cg + 31) >> 5;
+  const int n = tile / tiles_c, g0 = (tile - n * tiles_c) * 32;
+  const int g = g0 + (threadIdx.x >> 3), lane = threadIdx.x & 7;
   const int HW = d.H * d.W;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const T *p = X + (int64_t)n * HW * d.in_cs + d.in_co + g * 8;
-  for (int i = 0; i < HW; ++i) {
-    float x[8];
-    ld8_cg(p + (int64_t)i * d.in_cs, x);
+  if (g < cg) {
+    const T *p = X + (int64_t)n * HW * d.in_cs + d.in_co + g * 8;
+    int i = lane;
+    for (; i + 24 < HW; i += 32) {   // 4 independent loads in flight per thread
+      float x0[8], x1[8], x2[8], x3[8];
+      ld8_cg(p + (int64_t)i * d.in_cs, x0);
+      ld8_cg(p + (int64_t)(i + 8) * d.in_cs, x1);
+      ld8_cg(p + (int64_t)(i + 16) * d.in_cs, x2);
+      ld8_cg(p + (int64_t)(i + 24) * d.in_cs, x3);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] += x[q];
+      for (int q = 0; q < 8; ++q) acc[q] += ((x0[q] + x1[q]) + (x2[q] + x3[q]));
+    }
+    for (; i < HW; i += 8) {
+      float x[8];
+      ld8_cg(p + (int64_t)i * d.in_cs, x);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] += x[q];
+    }
   }
-  const float inv = 1.f / (float)HW;
+  float *red = reinterpret_cast<float *>(smem);   // [256][8]
 #pragma unroll
-  for (int q = 0; q < 8; ++q) acc[q] *= inv;
-  store_out8<T>(a, d, n, g * 8, acc, 8);
+  for (int q = 0; q < 8; ++q) red[threadIdx.x * 8 + q] = acc[q];
+  __syncthreads();
+  if (lane == 0 && g < cg) {
+    float s[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float *r = red + threadIdx.x * 8 + q;
+      s[q] = ((r[0] + r[8]) + (r[16] + r[24])) + ((r[32] + r[40]) + (r[48] + r[56]));
+    }
+    const float inv = 1.f / (float)HW;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s[q] *= inv;
+    store_out8<T>(a, d, n, g * 8, s, 8);
+  }
 }
 
 // ------------------------------------------------------------------------------------------
 // a8: FC (GEMV at b=1, skinny GEMM up to 8 columns per pass): one warp per output row, 16-byte
 // weight loads, lane-strided partial sums reduced by a fixed xor-shuffle tree (deterministic)
 // ------------------------------------------------------------------------------------------
+template <typename T, int NB>
+__device__ __forceinline__ void fc_rows(const OpDesc &d, const T *X, const T *Wr, int b0, int nb, int lane,
+                                        float *acc) {
+  const int K8 = d.K >> 3;
+  constexpr int U = NB == 1 ? 8 : 2;   // 16-byte weight loads in flight per lane
+  int k8 = lane;
+  for (; k8 + 32 * (U - 1) < K8; k8 += 32 * U) {
+    Raw8<T> wr[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) wr[u] = ldraw_nc(Wr + (int64_t)(k8 + 32 * u) * 8);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float w[8];
+      cvt8(wr[u], w);
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        if (NB == 1 || b < nb) {
+          float x[8];
+          ld8_cg(X + (int64_t)(b0 + b) * d.K + (int64_t)(k8 + 32 * u) * 8, x);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[b] = fmaf(w[q], x[q], acc[b]);
+        }
+      }
+    }
+  }
+  for (; k8 < K8; k8 += 32) {
+    float w[8];
+    ld8_nc(Wr + (int64_t)k8 * 8, w);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      if (NB == 1 || b < nb) {
+        float x[8];
+        ld8_cg(X + (int64_t)(b0 + b) * d.K + (int64_t)k8 * 8, x);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[b] = fmaf(w[q], x[q], acc[b]);
+      }
+    }
+  }
+}
+
 template <typename T>
 __device__ void fc_tile(const RunArgs &a, const OpDesc &d, int tile) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -585,24 +876,11 @@ __device__ void fc_tile(const RunArgs &a, const OpDesc &d, int tile) {
   const int nb = min(MT_FC_BATCH, d.N - b0);
   const T *X = in_ptr<T>(a, d);
   const T *Wr = reinterpret_cast<const T *>(d.w) + (int64_t)o * d.K;
-  const int K8 = d.K >> 3;
   float acc[MT_FC_BATCH];
 #pragma unroll
   for (int b = 0; b < MT_FC_BATCH; ++b) acc[b] = 0.f;
-#pragma unroll 4
-  for (int k8 = lane; k8 < K8; k8 += 32) {
-    float w[8];
-    ld8_nc(Wr + (int64_t)k8 * 8, w);
-#pragma unroll
-    for (int b = 0; b < MT_FC_BATCH; ++b) {
-      if (b < nb) {
-        float x[8];
-        ld8_cg(X + (int64_t)(b0 + b) * d.K + (int64_t)k8 * 8, x);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[b] = fmaf(w[q], x[q], acc[b]);
-      }
-    }
-  }
+  if (nb == 1) fc_rows<T, 1>(d, X, Wr, b0, 1, lane, acc);
+  else fc_rows<T, MT_FC_BATCH>(d, X, Wr, b0, nb, lane, acc);
 #pragma unroll
   for (int b = 0; b < MT_FC_BATCH; ++b) {
 #pragma unroll
@@ -623,13 +901,11 @@ __device__ void fc_tile(const RunArgs &a, const OpDesc &d, int tile) {
 template <typename T>
 __device__ void elt_tile(const RunArgs &a, const OpDesc &d, int tile) {
   const int cg = d.Co >> 3;
-  const int64_t items = (int64_t)d.N * d.Ho * d.Wo * cg;
-#pragma unroll
-  for (int e = 0; e < MT_EW_PER_THREAD; ++e) {
-    const int64_t it = (int64_t)tile * (MT_NTHREADS * MT_EW_PER_THREAD) + e * MT_NTHREADS + threadIdx.x;
-    if (it >= items) break;
-    const int64_t pix = it / cg;
-    const int g = (int)(it - pix * cg);
+  const int64_t p0 = (int64_t)tile * d.pix_tile;
+  const int64_t np = min((int64_t)d.pix_tile, (int64_t)d.N * d.Ho * d.Wo - p0);
+  for (int it = threadIdx.x; it < np * cg; it += MT_NTHREADS) {
+    const int64_t pix = p0 + it / cg;
+    const int g = it - (it / cg) * cg;
     float y[8];
     if (d.kind == 8) {  // ADD
       for (int q = 0; q < 8; ++q) y[q] = 0.f;
@@ -688,12 +964,66 @@ __device__ void run_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_t *s
       break;
     case TK_DW: if (f32) dw_tile<float>(a, d, tile); else dw_tile<bf16>(a, d, tile); break;
     case TK_POOL: if (f32) pool_tile<float>(a, d, tile); else pool_tile<bf16>(a, d, tile); break;
-    case TK_GAP: if (f32) gap_tile<float>(a, d, tile); else gap_tile<bf16>(a, d, tile); break;
+    case TK_GAP: if (f32) gap_tile<float>(a, d, tile, smem); else gap_tile<bf16>(a, d, tile, smem); break;
     case TK_FC: if (f32) fc_tile<float>(a, d, tile); else fc_tile<bf16>(a, d, tile); break;
     case TK_ELT: if (f32) elt_tile<float>(a, d, tile); else elt_tile<bf16>(a, d, tile); break;
     default: break;
   }
   __syncthreads();
+}
+
+// output pixel range [p0, p1) of a tile (pixel = n*Ho*Wo + ho*Wo + wo; FC/GAP: batch index)
+__device__ __forceinline__ void tile_out_range(const OpDesc &d, int tile, int64_t &p0, int64_t &p1) {
+  const int64_t npix = (int64_t)d.N * d.Ho * d.Wo;
+  switch (d.tk) {
+    case TK_CONV_TC: p0 = (int64_t)((tile / d.splits) / d.tiles_n) * MT_BM; p1 = p0 + MT_BM; break;
+    case TK_CONV_SIMT: p0 = (int64_t)(tile / d.tiles_n) * MT_SIMT_BM; p1 = p0 + MT_SIMT_BM; break;
+    case TK_GAP: p0 = tile / ((d.Co / 8 + 31) / 32); p1 = p0 + 1; break;
+    case TK_FC: p0 = (int64_t)(tile / ((d.Co + MT_FC_ROWS - 1) / MT_FC_ROWS)) * MT_FC_BATCH; p1 = p0 + MT_FC_BATCH; break;
+    default: p0 = (int64_t)tile * d.pix_tile; p1 = p0 + d.pix_tile; break;
+  }
+  if (p1 > npix) p1 = npix;
+}
+// input pixel range [i0, i1) the tile reads (receptive field, whole rows, clamped)
+__device__ __forceinline__ void tile_in_range(const OpDesc &d, int64_t p0, int64_t p1, int64_t &i0, int64_t &i1) {
+  const int64_t HW = (int64_t)d.H * d.W;
+  if (d.tk == TK_ELT) { i0 = p0; i1 = p1; return; }
+  if (d.tk == TK_GAP) { i0 = p0 * HW; i1 = p1 * HW; return; }
+  if (d.tk == TK_FC) { i0 = p0 * HW; i1 = p1 * HW; return; }
+  const int HoWo = d.Ho * d.Wo;
+  const int na = (int)(p0 / HoWo), nb = (int)((p1 - 1) / HoWo);
+  const int hoa = (int)((p0 - (int64_t)na * HoWo) / d.Wo), hob = (int)((p1 - 1 - (int64_t)nb * HoWo) / d.Wo);
+  const int ha = max(0, min(d.H - 1, hoa * d.sh - d.ph));
+  const int hb = max(0, min(d.H - 1, hob * d.sh - d.ph + d.kh - 1));
+  i0 = (int64_t)na * HW + (int64_t)ha * d.W;
+  i1 = (int64_t)nb * HW + (int64_t)(hb + 1) * d.W;
+}
+// completion block a finished tile contributes to (-1: none, e.g. a non-final split-K part)
+__device__ __forceinline__ int tile_block(const OpDesc &d, int tile, const CtaShared &sh) {
+  switch (d.tk) {
+    case TK_CONV_TC: return (d.splits == 1 || sh.last) ? (tile / d.splits) / d.tiles_n : -1;
+    case TK_CONV_SIMT: return tile / d.tiles_n;
+    case TK_GAP: return tile / ((d.Co / 8 + 31) / 32);
+    case TK_FC: return tile / ((d.Co + MT_FC_ROWS - 1) / MT_FC_ROWS);
+    default: return tile;
+  }
+}
+
+// work that needs no producer data: issued before the dependency wait so it overlaps it
+__device__ void tile_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaShared &sh, const PipeState &ps) {
+  if (d.tk == TK_CONV_TC) {
+    conv_tc_prefetch(d, tile, smem, sh, ps);
+  } else if (d.tk == TK_FC) {
+    const int rb = (int)(tile % ((d.Co + MT_FC_ROWS - 1) / MT_FC_ROWS));
+    const int o = rb * MT_FC_ROWS + (threadIdx.x >> 5);
+    if ((threadIdx.x & 31) == 0 && o < d.Co) {
+      const int eb = d.prec == 1 ? 4 : 2;
+      const char *row = reinterpret_cast<const char *>(d.w) + (int64_t)o * d.K * eb;
+      const int64_t bytes = (int64_t)d.K * eb;
+      for (int64_t off = 0; off < bytes; off += 65536)
+        prefetch_l2_bulk(row + off, (uint32_t)(bytes - off < 65536 ? bytes - off : 65536));
+    }
+  }
 }
 
 __device__ __forceinline__ void load_desc(CtaShared &sh, const OpDesc *src) {
@@ -768,7 +1098,30 @@ __device__ bool grid_barrier(const RunArgs &a, CtaShared &sh) {
   return sh.ok != 0;
 }
 
-// one stage: pick (op, tile) from the home tenant first, then the others; returns false on abort
+// debug trace record: op, tile, smid/cta, pick, deps-satisfied, mainloop-done, end timestamps
+__device__ __forceinline__ void trace_tile(const RunArgs &a, const CtaShared &sh, int op, int tile) {
+  if (!a.trace) return;
+  const unsigned i = atomicAdd(&a.ctl->trace_count, 1u);
+  if ((int)i >= a.trace_cap) return;
+  unsigned smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  unsigned long long *e = a.trace + (size_t)i * 8;
+  e[0] = ((unsigned long long)(unsigned)tile << 32) | (unsigned)op;
+  e[1] = ((unsigned long long)blockIdx.x << 32) | smid;
+  e[2] = sh.t_pick;
+  e[3] = sh.t_deps;
+  e[4] = sh.t_mma;
+  e[5] = sh.t_run + (unsigned long long)sh.last;   // after the release
+  e[6] = (unsigned long long)sh.home;
+  e[7] = sh.t_run;
+}
+
+// One stage.  Claim-then-wait: thread 0 claims the next unclaimed tile of the first op of its
+// home tenant's slice that still has unclaimed tiles (then of the other tenants, round-robin,
+// when stealing), i.e. one atomic per pick; tiles are claimed in op order per tenant, so every
+// dependency of a claimed tile is itself claimed by a running CTA and the wait always ends
+// (all CTAs co-resident).  While the dependencies finish, the tile's weights are already
+// streamed into shared memory / L2 (tile_prefetch).
 __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh, PipeState &ps) {
   const int T = a.n_tenants;
   const int tid = threadIdx.x;
@@ -782,60 +1135,85 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
   __syncthreads();
   while (true) {
     if (tid == 0) {
-      int op = -1, tile = 0, status = 0;  // status: 0 searching, 1 found, 2 stage exhausted, 3 abort
-      const unsigned long long t0 = gtimer();
-      unsigned spins = 0;
-      while (status == 0) {
-        bool all_done = true;
-        for (int q = 0; q < T && status == 0; ++q) {
-          if (!a.steal && q > 0) break;
-          const int t = (sh.home + q) % T;
-          while (sh.cur[t] < sh.end[t]) {
-            const int o = sh.cur[t];
-            const OpDesc *od = a.ops + o;
-            const int nd = __ldg(&od->n_dep);
-            bool ready = true;
-            for (int k = 0; k < nd; ++k) {
-              const int dep = __ldg(&od->deps[k]);
-              if (ld_acquire(a.done + dep) < __ldg(&od->dep_tiles[k])) { ready = false; break; }
-            }
-            if (!ready) { all_done = false; break; }  // tenant blocked on its chain
-            const int k = atomicAdd(a.claim + o, 1);
-            if (k < __ldg(&od->tiles)) { op = o; tile = k; status = 1; break; }
-            sh.cur[t] = o + 1;  // every tile of o claimed
-          }
-          if (status == 0 && sh.cur[t] < sh.end[t]) all_done = false;
-        }
-        if (status == 0 && all_done) status = 2;
-        if (status == 0) {
-          if ((++spins & 63) == 0) {
-            if (ld_acquire_u(&a.ctl->error)) status = 3;
-            else if (gtimer() - t0 > a.timeout_ns) { atomicExch(&a.ctl->error, 2u); status = 3; }
-          }
-          if (status == 0) __nanosleep(40);
+      int op = -1, tile = 0, ten = -1;
+      for (int q = 0; q < T && op < 0; ++q) {
+        if (!a.steal && q > 0) break;
+        const int t = (sh.home + q) % T;
+        while (sh.cur[t] < sh.end[t]) {
+          const int o = sh.cur[t];
+          const int k = atomicAdd(a.claim + o, 1);
+          if (k < __ldg(&a.ops[o].tiles)) { op = o; tile = k; ten = t; break; }
+          sh.cur[t] = o + 1;  // every tile of o is claimed
         }
       }
-      sh.op = status == 1 ? op : (status == 2 ? -1 : -2);
+      sh.op = op;
       sh.tile = tile;
+      sh.ten = ten;
+      sh.t_pick = gtimer();
+      sh.t_mma = 0;
     }
     __syncthreads();
     const int op = sh.op;
-    if (op == -1) return true;
-    if (op == -2) return false;
+    if (op < 0) return true;
     load_desc(sh, a.ops + op);
     __syncthreads();
-    run_tile(a, sh.d, sh.tile, smem, sh, ps);
+    tile_prefetch(sh.d, sh.tile, smem, sh, ps);
     if (tid == 0) {
-      __threadfence();
-      atomicAdd(a.done + op, 1);  // release: this tile's outputs are visible
+      // wait for exactly the producer pixel blocks this tile reads (tile-level dataflow between
+      // consecutive ops of a tenant); whole producer ops already seen complete are cached
+      int ok = 1;
+      const OpDesc &d = sh.d;
+      int64_t p0, p1, i0, i1;
+      tile_out_range(d, sh.tile, p0, p1);
+      tile_in_range(d, p0, p1, i0, i1);
+      const unsigned long long t0 = gtimer();
+      unsigned spins = 0;
+      for (int k = 0; k < d.n_dep && ok; ++k) {
+        const int dep = d.deps[k];
+        if (dep < 2048 && (sh.complete[dep >> 5] >> (dep & 31) & 1u)) continue;
+        const OpDesc *pd = a.ops + dep;
+        if (ld_acquire(a.done + dep) >= __ldg(&pd->tiles)) {
+          if (dep < 2048) sh.complete[dep >> 5] |= 1u << (dep & 31);
+          continue;
+        }
+        int64_t lo = INT64_MAX, hi = 0;
+        if (d.dep_kind[k] & 1) { lo = i0; hi = i1; }
+        if (d.dep_kind[k] & 2) { lo = min(lo, p0); hi = max(hi, p1); }
+        const int pb = __ldg(&pd->pix_blk), need = __ldg(&pd->blk_need), off = __ldg(&pd->blk_off);
+        const int nbk = __ldg(&pd->nblk);
+        const int b0 = (int)(lo / pb), b1 = min(nbk - 1, (int)((hi - 1) / pb));
+        for (int b = b0; b <= b1 && ok; ++b) {
+          while (ld_acquire(a.blkcnt + off + b) < need) {
+            if ((++spins & 255) == 0) {
+              if (ld_acquire_u(&a.ctl->error)) { ok = 0; break; }
+              if (gtimer() - t0 > a.timeout_ns) { atomicExch(&a.ctl->error, 2u); ok = 0; break; }
+            }
+            __nanosleep(20);
+          }
+        }
+      }
+      sh.ok = ok;
+      sh.t_deps = gtimer();
+    }
+    __syncthreads();
+    if (!sh.ok) { cp_async_wait<0>(); return false; }
+    run_tile(a, sh.d, sh.tile, smem, sh, ps);
+    if (tid == 0) {   // publish: this tile's outputs are visible (release)
+      sh.t_run = gtimer();
+      const int b = tile_block(sh.d, sh.tile, sh);
+      if (b >= 0) red_release_add(a.blkcnt + sh.d.blk_off + b, 1);
+      red_release_add(a.done + op, 1);
+      if (a.trace) sh.last = (int)(gtimer() - sh.t_run);
+      trace_tile(a, sh, op, sh.tile);
     }
   }
 }
 
 __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
   uint8_t *smem = smem_base();
-  CtaShared &sh = *reinterpret_cast<CtaShared *>(smem + PIPE_BYTES);
+  __shared__ __align__(16) CtaShared sh;
   PipeState ps{0u, 0u};
+  if (threadIdx.x < 64) sh.complete[threadIdx.x] = 0u;
   cta_setup(sh, true);
   bool ok = grid_barrier(a, sh);
   if (ok) {
@@ -863,6 +1241,8 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
       a.claim[i] = 0;
       a.done[i] = 0;
     }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_blk; i += gridDim.x * blockDim.x)
+      a.blkcnt[i] = 0;
   }
   cta_teardown(sh, true);
 }
@@ -870,25 +1250,37 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
 // baseline: all tiles of one op, grid-strided
 __global__ void __launch_bounds__(MT_NTHREADS, 1) op_kernel(RunArgs a, int op) {
   uint8_t *smem = smem_base();
-  CtaShared &sh = *reinterpret_cast<CtaShared *>(smem + PIPE_BYTES);
+  __shared__ __align__(16) CtaShared sh;
   PipeState ps{0u, 0u};
   load_desc(sh, a.ops + op);
   const bool tc = __ldg(&a.ops[op].tk) == TK_CONV_TC;
   cta_setup(sh, tc);
-  for (int t = blockIdx.x; t < sh.d.tiles; t += gridDim.x) run_tile(a, sh.d, t, smem, sh, ps);
+  for (int t = blockIdx.x; t < sh.d.tiles; t += gridDim.x) {
+    if (threadIdx.x == 0) { sh.t_pick = gtimer(); sh.t_mma = 0; sh.home = -1; }
+    tile_prefetch(sh.d, t, smem, sh, ps);
+    if (threadIdx.x == 0) sh.t_deps = gtimer();
+    run_tile(a, sh.d, t, smem, sh, ps);
+    if (threadIdx.x == 0) trace_tile(a, sh, op, t);
+  }
   cta_teardown(sh, tc);
 }
 
 // small-smem variant for non-tensor-core ops so several op kernels can share an SM
-static constexpr int SMALL_SMEM = 1024 + MT_SIMT_BK * (MT_SIMT_BM + MT_SIMT_BN) * 4 + ((sizeof(CtaShared) + 127) / 128) * 128;
+static constexpr int SMALL_SMEM = 1024 + MT_SIMT_BK * (MT_SIMT_BM + MT_SIMT_BN) * 4;
 __global__ void __launch_bounds__(MT_NTHREADS) op_kernel_small(RunArgs a, int op) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  CtaShared &sh = *reinterpret_cast<CtaShared *>(smem + MT_SIMT_BK * (MT_SIMT_BM + MT_SIMT_BN) * 4);
+  __shared__ __align__(16) CtaShared sh;
   PipeState ps{0u, 0u};
   load_desc(sh, a.ops + op);
   __syncthreads();
-  for (int t = blockIdx.x; t < sh.d.tiles; t += gridDim.x) run_tile(a, sh.d, t, smem, sh, ps);
+  for (int t = blockIdx.x; t < sh.d.tiles; t += gridDim.x) {
+    if (threadIdx.x == 0) { sh.t_pick = gtimer(); sh.t_mma = 0; sh.home = -1; }
+    tile_prefetch(sh.d, t, smem, sh, ps);
+    if (threadIdx.x == 0) sh.t_deps = gtimer();
+    run_tile(a, sh.d, t, smem, sh, ps);
+    if (threadIdx.x == 0) trace_tile(a, sh, op, t);
+  }
 }
 
 __global__ void pack_kernel(RunArgs a, int t) {

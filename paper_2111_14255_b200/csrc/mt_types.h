@@ -44,7 +44,11 @@ struct OpDesc {
   int32_t in_cs, in_co, out_cs, out_co;
   int32_t res_cs, res_co, ins_cs[MT_MAXIN], ins_co[MT_MAXIN];
   int32_t deps[MT_MAXDEP];          // global op ids this op reads
-  int32_t dep_tiles[MT_MAXDEP];     // tile counts of those ops (dependency satisfied when done == tiles)
+  int32_t dep_kind[MT_MAXDEP];      // bit 0: read as input, bit 1: read as residual
+  // completion tracking: output pixels (N*Ho*Wo, FC/GAP: batch index) are split into blocks of
+  // pix_blk; block b of this op is complete when blkcnt[blk_off + b] == blk_need
+  int32_t pix_blk, blk_need, nblk, blk_off;
+  int32_t pix_tile;                 // pointwise tiles: output pixels per tile
   int32_t pad1;
   int32_t M, K, Kpad, nkb;          // GEMM view (conv / FC)
   int32_t bn, tiles_m, tiles_n, splits;
@@ -58,7 +62,7 @@ struct CtlBlock {
   unsigned int bar_count;
   unsigned int bar_gen;
   unsigned int error;        // nonzero: a spin timed out / invariant broken
-  unsigned int pad;
+  unsigned int trace_count;  // entries written to the trace buffer
   unsigned long long err_info;
 };
 
@@ -68,12 +72,15 @@ struct RunArgs {
   const uint8_t *home;       // [S][grid] home tenant of each CTA
   int32_t n_stages, n_tenants, steal, n_pack;
   int32_t *claim;            // [n_ops] tile claim counters
-  int32_t *done;             // [n_ops] finished-tile counters
+  int32_t *done;             // [n_ops] completed-tile counters
+  int32_t *blkcnt;           // [total blocks] completed-tile counters per output pixel block
   int32_t *splitcnt;         // split-K arrival counters
   CtlBlock *ctl;
   unsigned long long *ts;    // [n_stages + 2] %globaltimer stamps (or NULL)
   unsigned long long timeout_ns;
-  int32_t n_ops, ts_full;     // ts_full: 1 = all stage stamps, 0 = start/end only
+  int32_t n_ops, ts_full;
+  int32_t n_blk, trace_cap;
+  unsigned long long *trace; // [trace_cap][8] per-tile records (debug; NULL = off)     // ts_full: 1 = all stage stamps, 0 = start/end only
   const float *inputs[MT_MAXT];     // per tenant user input (NCHW fp32)
   float *outputs[MT_MAXT];          // per tenant user output (fp32)
   uint64_t packed[MT_MAXT];         // per tenant packed-input buffer (NHWC, C padded)

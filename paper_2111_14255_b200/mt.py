@@ -75,6 +75,8 @@ _sig = {
     "mt_profile_batch_pointers": (C.c_int, [P, C.c_int32, I32P, I32P, C.POINTER(P), C.POINTER(P),
                                             C.c_int32, C.c_int32, F32P, I32P, P]),
     "mt_get_activation": (C.c_int, [P, C.c_int32, C.c_int32, P, C.c_size_t]),
+    "mt_set_trace": (C.c_int, [P, P, C.c_int64]),
+    "mt_trace_count": (C.c_int, [P, C.POINTER(C.c_int64)]),
     "mt_last_error_info": (C.c_int, [P, C.POINTER(mt_error_info)]),
     "mt_last_error": (C.c_char_p, [P]),
     "mt_version": (C.c_char_p, []),
@@ -272,6 +274,14 @@ class Context:
                                     _ptrs(in_ptrs), _ptrs(out_ptrs), warmup, iters,
                                     lat.ctypes.data_as(F32P), st.ctypes.data_as(I32P), P(stream)))
         return lat, st
+
+    def set_trace(self, dev_ptr, capacity):
+        self.check(mt_set_trace(self.h, P(int(dev_ptr) if dev_ptr else 0), int(capacity)))
+
+    def trace_count(self):
+        v = C.c_int64()
+        self.check(mt_trace_count(self.h, C.byref(v)))
+        return v.value
 
     def get_activation(self, t, j, shape_nhwc, dtype):
         buf = np.zeros(shape_nhwc, dtype=dtype)

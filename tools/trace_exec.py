@@ -1,0 +1,92 @@
+"""Per-tile trace of one executor run (mt_set_trace): where does the time go?
+
+  python tools/trace_exec.py --config c2 [--schedule all_concurrent] [--baseline seq] [--out f.json]
+"""
+import argparse
+import collections
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2111_14255_b200.session import TenantMix  # noqa: E402
+from workloads import configs, zoo  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--schedule", default="all_concurrent")
+ap.add_argument("--baseline", default=None)
+ap.add_argument("--out", default=None)
+ap.add_argument("--top", type=int, default=30)
+ap.add_argument("--synthetic", default=None, help="dwchain | pwchain | gapchain")
+a = ap.parse_args()
+if a.synthetic:
+    b = zoo.GraphBuilder("tinyA", 1, 384, 14, 14, zoo.PREC_BF16, seed=0)
+    x = b.conv(-1, 384, 1, 1, 0)
+    for i in range(12):
+        if a.synthetic == "dwchain":
+            x = b.conv(x, 384, 3, 1, 1, groups=384)
+        elif a.synthetic == "pwchain":
+            x = b.conv(x, 384, 1, 1, 0)
+        else:
+            x = b.relu(x)
+    b.gap(x)
+    g = [b.build()]
+else:
+    g = configs.tenants(a.config)
+L = [x.n_ops for x in g]
+m = TenantMix(g)
+m.set_input(zoo.make_input(g[0]))
+rho = {"all_concurrent": configs.all_concurrent_pointers, "sequential": configs.sequential_pointers,
+       "uniform4": configs.uniform_pointers}[a.schedule](L)
+m.ctx.set_schedule_pointers(rho)
+for _ in range(3):
+    m.run()
+cap = 1 << 16
+buf = torch.zeros(cap * 8, dtype=torch.int64, device="cuda")
+m.ctx.set_trace(buf.data_ptr(), cap)
+if a.baseline:
+    total = m.ctx.run_baseline(a.baseline, m.in_ptrs, m.out_ptrs)
+    stages = []
+else:
+    total, stages = m.run()
+n = m.ctx.trace_count()
+m.ctx.set_trace(0, 0)
+tr = buf[: n * 8].view(n, 8).cpu().numpy().astype(np.int64)
+t0 = tr[:, 2].min()
+names = []
+for t, gg in enumerate(g):
+    for j in range(gg.n_ops):
+        nd = gg.nodes[j]
+        names.append(f"{gg.name[:8]}:{j}:{zoo.KIND_NAMES[nd['kind']]}{'dw' if nd['groups'] > 1 else ''}"
+                     f"{nd['kh']}x{nd['kw']}s{nd['sh']}->{gg.shapes[j]}")
+per = collections.defaultdict(list)
+for r in tr:
+    per[int(r[0] & 0xffffffff)].append(r)
+rows = []
+for op, rs in per.items():
+    rs = np.array(rs)
+    wait = (rs[:, 3] - rs[:, 2]) / 1e3
+    work = (rs[:, 5] - rs[:, 3]) / 1e3
+    mma = np.where(rs[:, 4] > 0, (rs[:, 4] - rs[:, 3]) / 1e3, 0)
+    run = (rs[:, 7] - rs[:, 3]) / 1e3
+    rel = (rs[:, 5] - rs[:, 7]) / 1e3
+    span = (rs[:, 5].max() - rs[:, 2].min()) / 1e3
+    rows.append(dict(op=op, name=names[op], tiles=len(rs), start=(rs[:, 2].min() - t0) / 1e3,
+                     end=(rs[:, 5].max() - t0) / 1e3, span=span, wait_mean=wait.mean(), wait_max=wait.max(),
+                     work_mean=work.mean(), work_max=work.max(), mma_mean=mma.mean(),
+                     run_mean=run.mean(), rel_mean=rel.mean()))
+rows.sort(key=lambda r: r["start"])
+print(f"total {total:.1f} us, stages {[round(s, 1) for s in stages]}, tiles traced {n}")
+print(f"{'op':>4} {'name':46} {'tiles':>5} {'start':>7} {'end':>7} {'wait':>6} {'work':>6} {'wmax':>6} {'mma':>6} {'run':>6} {'rel':>6}")
+for r in rows:
+    print(f"{r['op']:4d} {r['name'][:46]:46} {r['tiles']:5d} {r['start']:7.1f} {r['end']:7.1f} {r['wait_mean']:6.2f} "
+          f"{r['work_mean']:6.2f} {r['work_max']:6.2f} {r['mma_mean']:6.2f} {r['run_mean']:6.2f} {r['rel_mean']:6.2f}")
+busy = ((tr[:, 5] - tr[:, 3]).sum() / 1e3)
+print(f"SM-busy (work) us summed over CTAs: {busy:.1f}; makespan x CTAs: {total * 148:.1f} -> util {busy / (total * 148):.3f}")
+if a.out:
+    json.dump(dict(total=total, stages=stages, rows=rows), open(a.out, "w"), indent=1)
