@@ -1,5 +1,6 @@
 // libmt.so host runtime: C ABI (include/mt.h), graph ingest (a1), tile plans + stage plans (a3),
 // workspace layout, executor / baseline / profiling launches (a4, a9, a10).
+#include <cuda.h>  // CUtensorMap types only; the driver is reached via cudaGetDriverEntryPoint
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -369,33 +370,50 @@ static mt_status plan_graphs(mt_ctx *c) {
               // whole output rows per tile (row-run kernel): ~MT_NTHREADS*1.5 items per tile
               const int run = n.sh == 1 ? 4 : 2;
               const int64_t per_row = cdiv(os.w, run) * (os.c / 8);
-              const int rows = (int)std::max<int64_t>(1, (MT_NTHREADS * 3 / 2) / per_row);
+              const int rows = (int)std::max<int64_t>(1, MT_NTHREADS / per_row);
               d.pix_tile = rows * os.w;
             } else {
               d.pix_tile = (int)std::max<int64_t>(1, (MT_NTHREADS * MT_EW_PER_THREAD) / (os.c / 8));
             }
             d.tiles = (int)cdiv((int64_t)g.batch * os.h * os.w, d.pix_tile);
             wp.mode = 3;
-            wp.bytes = (int64_t)n.kh * n.kw * os.c * eb;
+            wp.bytes = (int64_t)n.kh * n.kw * os.c * 4;   // fp32 (tiny; saves conversions)
           } else if (bf16) {
             d.tk = TK_CONV_TC;
             d.M = g.batch * os.h * os.w;
-            d.K = n.kh * n.kw * d.C;
-            d.Kpad = (int)rup(d.K, MT_BK);
-            d.nkb = d.Kpad / MT_BK;
             d.bn = os.c <= 16 ? 16 : os.c <= 32 ? 32 : os.c <= 64 ? 64 : 128;
-            d.tiles_m = (int)cdiv(d.M, MT_BM);
             d.tiles_n = (int)cdiv(os.c, d.bn);
+            // TMA mainloop: whole output rows per M tile; a K-block is one tap x 64 channels, loaded
+            // as one 4-D box {64 ch, Wo*sw, R*sh, 1} with element strides {1, sw, sh, 1}
+            const int Rrows = std::min(os.h, 128 / std::max(os.w, 1));
+            if (!iv.graph_in && d.C >= 16 && os.w <= 128 && os.w * n.sw <= 256 && Rrows >= 1 &&
+                Rrows * n.sh <= 256) {
+              d.tma = 1;
+              d.blk_rows = Rrows;
+              d.blk_tpi = (int)cdiv(os.h, Rrows);
+              d.tiles_m = g.batch * d.blk_tpi;
+              d.cblks = (int)cdiv(d.C, 64);
+              d.nkb = n.kh * n.kw * d.cblks;
+              d.Kpad = d.nkb * MT_BK;
+              d.K = d.Kpad;
+              d.a_bytes = Rrows * os.w * 128;
+            } else {
+              d.K = n.kh * n.kw * d.C;
+              d.Kpad = (int)rup(d.K, MT_BK);
+              d.nkb = d.Kpad / MT_BK;
+              d.tiles_m = (int)cdiv(d.M, MT_BM);
+            }
             const int tmn = d.tiles_m * d.tiles_n;
             int splits = 1;
             if (tmn < 74 && d.nkb >= 8) {
-              splits = (int)std::min<int64_t>(std::min<int64_t>(cdiv(148, tmn), d.nkb / 4), 16);
+              splits = (int)std::min<int64_t>(std::min<int64_t>(cdiv(148, tmn), d.nkb / 4), 12);
               splits = std::max(splits, 1);
             }
             d.kb_per_split = (int)cdiv(d.nkb, splits);
             d.splits = (int)cdiv(d.nkb, d.kb_per_split);
-            d.tiles = tmn * d.splits;
-            wp.mode = 1;
+            d.rc = d.splits > 1 ? std::max(1, d.bn / 32) : 0;
+            d.tiles = tmn * d.splits + tmn * d.rc;
+            wp.mode = d.tma ? 5 : 1;
             wp.bytes = (int64_t)d.tiles_n * d.bn * d.Kpad * 2;
             if (d.splits > 1) {
               d.cnt_off = split_cnt;
@@ -456,13 +474,16 @@ static mt_status plan_graphs(mt_ctx *c) {
     OpDesc &d = h.d;
     const int64_t npix = (int64_t)d.N * d.Ho * d.Wo;
     switch (d.tk) {
-      case TK_CONV_TC: d.pix_blk = MT_BM; d.blk_need = d.tiles_n; break;
+      case TK_CONV_TC:   // (blk_rows for TMA); split-K: the reduce tiles complete the block
+        d.pix_blk = MT_BM;
+        d.blk_need = d.tiles_n * (d.splits > 1 ? d.rc : 1);
+        break;
       case TK_CONV_SIMT: d.pix_blk = MT_SIMT_BM; d.blk_need = d.tiles_n; break;
       case TK_GAP: d.pix_blk = 1; d.blk_need = (int)cdiv(d.Co / 8, 32); break;
       case TK_FC: d.pix_blk = MT_FC_BATCH; d.blk_need = (int)cdiv(d.Co, MT_FC_ROWS); break;
       default: d.pix_blk = d.pix_tile; d.blk_need = 1; break;
     }
-    d.nblk = (int)cdiv(npix, d.pix_blk);
+    d.nblk = d.blk_rows > 0 ? d.N * d.blk_tpi : (int)cdiv(npix, d.pix_blk);
     d.blk_off = (int)nblk_total;
     nblk_total += d.nblk;
   }
@@ -487,6 +508,7 @@ static mt_status plan_graphs(mt_ctx *c) {
   L.splitcnt = take(sizeof(int32_t) * std::max(split_cnt, 1));
   L.counters_bytes = off;
   L.ops = take(sizeof(OpDesc) * total);
+  L.tmaps = take((size_t)256 * total);
   L.sched_rng = take(sizeof(int32_t) * S_max * NT * 2);
   L.sched_home = take((size_t)S_max * c->grid);
   L.prof_area_bytes = 8u << 20;
@@ -645,6 +667,62 @@ static mt_status check_device_error(mt_ctx *c) {
     cudaDeviceSynchronize();
     return fail(c, MT_ERR_INTERNAL, m);
   }
+  return MT_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// TMA tensor maps (cuTensorMapEncodeTiled through the runtime's driver entry point)
+// ------------------------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                      const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                      const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t encode_fn() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled_t)p;
+  }
+  return fn;
+}
+
+// A: activations NHWC viewed as 4-D {C, W, H, N} (channel slice of a possibly concatenated
+// buffer); box {64, Wo*sw, R*sh, 1} with traversal strides {1, sw, sh, 1} = the im2col rows of one
+// tap for R whole output rows; out-of-range coordinates (padding) are zero-filled by the TMA unit.
+// B: packed weights {Kpad, Cout_pad}, box {64, bn}.  Both 128-byte swizzled (UMMA SW128 K-major).
+static mt_status make_conv_tmaps(mt_ctx *c, const OpDesc &o, const HostOp &h, char *ma_dev, char *mb_dev) {
+  PFN_encodeTiled_t enc = encode_fn();
+  if (!enc) return fail(c, MT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  alignas(64) CUtensorMap ma, mb;
+  const cuuint64_t es = 2;
+  cuuint64_t gdim[4] = {(cuuint64_t)o.C, (cuuint64_t)o.W, (cuuint64_t)o.H, (cuuint64_t)o.N};
+  cuuint64_t gstr[3] = {(cuuint64_t)o.in_cs * es, (cuuint64_t)o.W * o.in_cs * es,
+                        (cuuint64_t)o.H * o.W * o.in_cs * es};
+  cuuint32_t box[4] = {64, (cuuint32_t)(o.Wo * o.sw), (cuuint32_t)(o.blk_rows * o.sh), 1};
+  cuuint32_t estr[4] = {1, (cuuint32_t)o.sw, (cuuint32_t)o.sh, 1};
+  void *base = (void *)(o.in + (uint64_t)o.in_co * es);
+  CUresult r = enc(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, gdim, gstr, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char m[160];
+    snprintf(m, sizeof m, "tensor map A (op %d) encode failed: %d", (int)(&h - c->ops.data()), (int)r);
+    return fail(c, MT_ERR_CUDA, m);
+  }
+  cuuint64_t bdim[2] = {(cuuint64_t)o.Kpad, (cuuint64_t)o.tiles_n * o.bn};
+  cuuint64_t bstr[1] = {(cuuint64_t)o.Kpad * es};
+  cuuint32_t bbox[2] = {64, (cuuint32_t)o.bn};
+  cuuint32_t bes[2] = {1, 1};
+  r = enc(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void *)o.w, bdim, bstr, bbox, bes,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(c, MT_ERR_CUDA, "tensor map B encode failed");
+  CK(cudaMemcpy(ma_dev, &ma, sizeof ma, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(mb_dev, &mb, sizeof mb, cudaMemcpyHostToDevice));
   return MT_OK;
 }
 
@@ -811,6 +889,13 @@ mt_status mt_bind_workspace(mt_ctx *c, void *dev, size_t bytes) {
     o.ws = h.ws_off >= 0 ? (uint64_t)(c->ws + L.partials + h.ws_off) : 0;
     o.scale = (uint64_t)h.scale;
     o.shift = (uint64_t)h.shift;
+    if (o.tma) {
+      char *ma = c->ws + L.tmaps + 256 * i, *mb = ma + 128;
+      mt_status st = make_conv_tmaps(c, o, h, ma, mb);
+      if (st != MT_OK) return st;
+      o.tmap_a = (uint64_t)ma;
+      o.tmap_b = (uint64_t)mb;
+    }
     h.d = o;
     d[i] = o;
   }

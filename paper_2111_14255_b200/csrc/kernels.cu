@@ -31,6 +31,7 @@ static constexpr int PIPE_BYTES = MT_STAGES * (A_STAGE + B_STAGE);
 static constexpr int TMEM_COLS = 128;
 
 struct CtaShared {
+  unsigned long long bar_full[MT_STAGES];    // TMA: stage loaded (expect_tx)
   unsigned long long bar_empty[MT_STAGES];
   unsigned long long bar_accf;
   uint32_t tmem_base;
@@ -46,6 +47,7 @@ static constexpr int SMEM_BYTES = 1024 + PIPE_BYTES;   // + static __shared__ Ct
 struct PipeState {
   uint32_t fill;       // k-blocks loaded so far by this CTA (stage ring position)
   uint32_t acc_phase;  // parity of the accumulator-ready barrier
+  uint32_t fullph;     // bit s: parity of the next phase of the TMA full barrier of stage s
 };
 
 // ------------------------------------------------------------------------------------------
@@ -77,6 +79,21 @@ __device__ __forceinline__ void red_release_add(int *p, int v) {
 }
 __device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, uint64_t tmap, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, uint64_t tmap, uint32_t bar, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
 }
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
@@ -284,41 +301,52 @@ __device__ __forceinline__ void store_out8(const RunArgs &a, const OpDesc &d, in
 // Deterministic split-K: fp32 partials in workspace, the last-arriving CTA sums them in split
 // order 0..S-1 and runs the epilogue.
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ void conv_epilogue_vals(const RunArgs &a, const OpDesc &d, const CtaShared &sh,
-                                                   int m, int n0, int col, float *v) {
-  const int n = n0 + col;
-  const int nvalid = min(8, d.Co - n);
-  float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (d.flags & OPF_RES) {
-    const bf16 *rp = reinterpret_cast<const bf16 *>(d.res) + (int64_t)m * d.res_cs + d.res_co + n;
-    if (nvalid == 8) ld8_cg(rp, r);
-    else
-      for (int e = 0; e < nvalid; ++e) r[e] = ld1_cg(rp + e);
-  }
-#pragma unroll
-  for (int e = 0; e < 8; ++e) v[e] = act_f(fmaf(v[e], sh.esc[col + e], sh.esh[col + e]) + r[e], d.act);
-  store_out8<bf16>(a, d, m, n, v, nvalid);
-}
-
 struct ConvTile {
-  int tmn, ks, m0, n0, kb0, nk;
+  int tmn, ks, mt, m0, n0, kb0, nk;
+  int img, ho0;   // TMA path: image and first output row of the M tile
 };
 __device__ __forceinline__ ConvTile conv_tile_coords(const OpDesc &d, int tile) {
   ConvTile c;
   const int S = d.splits;
   c.tmn = tile / S;
   c.ks = tile - c.tmn * S;
-  const int mt = c.tmn / d.tiles_n, nt = c.tmn - (c.tmn / d.tiles_n) * d.tiles_n;
-  c.m0 = mt * MT_BM;
+  c.mt = c.tmn / d.tiles_n;
+  const int nt = c.tmn - c.mt * d.tiles_n;
+  c.m0 = c.mt * MT_BM;
   c.n0 = nt * d.bn;
   c.kb0 = c.ks * d.kb_per_split;
   c.nk = min(d.nkb, c.kb0 + d.kb_per_split) - c.kb0;
+  if (d.tma) {
+    c.img = c.mt / d.blk_tpi;
+    c.ho0 = (c.mt - c.img * d.blk_tpi) * d.blk_rows;
+  } else {
+    c.img = 0;
+    c.ho0 = 0;
+  }
   return c;
 }
+// output pixel of accumulator row r (TMEM lane), or -1 if the row is padding
+__device__ __forceinline__ int conv_row_pixel(const OpDesc &d, const ConvTile &c, int r) {
+  if (d.tma) {
+    const int hl = r / d.Wo;
+    const int ho = c.ho0 + hl;
+    if (hl >= d.blk_rows || ho >= d.Ho) return -1;
+    return (c.img * d.Ho + ho) * d.Wo + (r - hl * d.Wo);
+  }
+  const int m = c.m0 + r;
+  return m < d.M ? m : -1;
+}
+// TMA: issue the A box of k-block kb (one tap, 64 channels) for this M tile
+__device__ __forceinline__ void tma_issue_a(const OpDesc &d, const ConvTile &c, int kb, uint32_t dst, uint32_t bar) {
+  const int tap = kb / d.cblks, cb = kb - tap * d.cblks;
+  const int r = tap / d.kw, s = tap - r * d.kw;
+  tma_load_4d(dst, d.tmap_a, bar, cb * 64, s - d.pw, c.ho0 * d.sh + r - d.ph, c.img);
+}
 
-// Issue the weight (B) tiles of the first min(nk, MT_STAGES) k-blocks and stage the epilogue
-// constants.  Needs no producer data, so the executor runs it BEFORE waiting for the tile's
-// dependencies: the weight stream overlaps the wait.  Each k-block is its own commit group.
+// Work that needs no producer data, issued BEFORE the tile waits for its dependencies so the weight
+// stream overlaps the wait: the weight (B) tiles of the first min(nk, MT_STAGES) k-blocks and the
+// epilogue constants.  TMA path: thread 0 arms each stage's full barrier for A+B bytes and issues
+// B; A follows once the producers are complete.  cp.async path: one commit group per k-block.
 __device__ void conv_tc_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaShared &sh,
                                  const PipeState &ps) {
   const int tid = threadIdx.x;
@@ -326,20 +354,33 @@ __device__ void conv_tc_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaSh
   const bf16 *Wt = reinterpret_cast<const bf16 *>(d.w);
   const uint32_t sB = smem_u32(smem) + MT_STAGES * A_STAGE;
   const uint32_t bar_empty0 = smem_u32(&sh.bar_empty[0]);
-  const int c = tid & 7;
-  for (int i = 0; i < MT_STAGES; ++i) {
-    if (i < ct.nk) {
-      const uint32_t f = ps.fill + i;
-      const int s = f % MT_STAGES;
-      if (f >= MT_STAGES) mbar_wait(bar_empty0 + 8 * s, ((f / MT_STAGES) - 1) & 1);
-      const int kb = ct.kb0 + i;
-      const uint32_t sb = sB + s * B_STAGE;
-      for (int row = tid >> 3; row < d.bn; row += 32) {
-        const bf16 *src = Wt + (int64_t)(ct.n0 + row) * d.Kpad + kb * MT_BK + c * 8;
-        cp_async16(sb + row * 128 + ((c ^ (row & 7)) << 4), src, true);
+  if (d.tma) {
+    if (tid == 0) {
+      const uint32_t bar_full0 = smem_u32(&sh.bar_full[0]);
+      for (int i = 0; i < MT_STAGES && i < ct.nk; ++i) {
+        const uint32_t f = ps.fill + i;
+        const int s = f % MT_STAGES;
+        if (f >= MT_STAGES) mbar_wait(bar_empty0 + 8 * s, ((f / MT_STAGES) - 1) & 1);
+        mbar_expect_tx(bar_full0 + 8 * s, (uint32_t)(d.a_bytes + d.bn * 128));
+        tma_load_2d(sB + s * B_STAGE, d.tmap_b, bar_full0 + 8 * s, (ct.kb0 + i) * MT_BK, ct.n0);
       }
     }
-    cp_async_commit();
+  } else {
+    const int c = tid & 7;
+    for (int i = 0; i < MT_STAGES; ++i) {
+      if (i < ct.nk) {
+        const uint32_t f = ps.fill + i;
+        const int s = f % MT_STAGES;
+        if (f >= MT_STAGES) mbar_wait(bar_empty0 + 8 * s, ((f / MT_STAGES) - 1) & 1);
+        const int kb = ct.kb0 + i;
+        const uint32_t sb = sB + s * B_STAGE;
+        for (int row = tid >> 3; row < d.bn; row += 32) {
+          const bf16 *src = Wt + (int64_t)(ct.n0 + row) * d.Kpad + kb * MT_BK + c * 8;
+          cp_async16(sb + row * 128 + ((c ^ (row & 7)) << 4), src, true);
+        }
+      }
+      cp_async_commit();
+    }
   }
   if (tid < d.bn) {
     const int n = ct.n0 + tid;
@@ -352,16 +393,58 @@ __device__ void conv_tc_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaSh
                      (uint32_t)(ct.nk - MT_STAGES) * MT_BK * 2);
 }
 
-__device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_t *smem,
-                             CtaShared &sh, PipeState &ps) {
+// TMA mainloop: thread 0 = producer (A boxes, and B beyond the prefetched stages), thread 32 =
+// MMA issuer (UMMA 128 x bn x 16 from the two SW128 stages, commit frees the stage), everyone
+// else waits for the accumulator.
+__device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const ConvTile &ct, uint8_t *smem,
+                                                     CtaShared &sh, PipeState &ps) {
   const int tid = threadIdx.x;
-  const int S = d.splits;
-  const ConvTile ct = conv_tile_coords(d, tile);
-  const int tmn = ct.tmn, ks = ct.ks, m0 = ct.m0, n0 = ct.n0, kb0 = ct.kb0, nk = ct.nk;
+  const uint32_t sA = smem_u32(smem), sB = sA + MT_STAGES * A_STAGE;
+  const uint32_t bar_full0 = smem_u32(&sh.bar_full[0]);
+  const uint32_t bar_empty0 = smem_u32(&sh.bar_empty[0]);
+  const uint32_t bar_accf = smem_u32(&sh.bar_accf);
+  if (tid == 0) {
+    for (int i = 0; i < ct.nk; ++i) {
+      const uint32_t f = ps.fill + i;
+      const int s = f % MT_STAGES;
+      if (i >= MT_STAGES) {
+        mbar_wait(bar_empty0 + 8 * s, ((f / MT_STAGES) - 1) & 1);
+        mbar_expect_tx(bar_full0 + 8 * s, (uint32_t)(d.a_bytes + d.bn * 128));
+        tma_load_2d(sB + s * B_STAGE, d.tmap_b, bar_full0 + 8 * s, (ct.kb0 + i) * MT_BK, ct.n0);
+      }
+      tma_issue_a(d, ct, ct.kb0 + i, sA + s * A_STAGE, bar_full0 + 8 * s);
+    }
+  } else if (tid == 32) {
+    const uint32_t idesc = idesc_bf16(d.bn);
+    const uint32_t tmem = sh.tmem_base;
+    uint32_t ph = ps.fullph;
+    for (int i = 0; i < ct.nk; ++i) {
+      const uint32_t f = ps.fill + i;
+      const int s = f % MT_STAGES;
+      mbar_wait(bar_full0 + 8 * s, (ph >> s) & 1);
+      ph ^= 1u << s;
+      tc_fence_after();
+      const uint32_t ab = sA + s * A_STAGE, bb = sB + s * B_STAGE;
+#pragma unroll
+      for (int kk = 0; kk < MT_BK / 16; ++kk)
+        tc_mma(tmem, sdesc_sw128(ab + kk * 32), sdesc_sw128(bb + kk * 32), idesc, (i > 0 || kk > 0) ? 1u : 0u);
+      tc_commit(bar_empty0 + 8 * s);
+    }
+    tc_commit(bar_accf);
+  }
+}
+
+// cp.async mainloop (small-channel convs, e.g. the 3->8-padded stems): all threads gather im2col
+// rows, commit groups: MT_STAGES B-prefetch groups (conv_tc_prefetch) precede the loop's groups;
+// group NS + j holds A (and, for j >= NS, B) of k-block j, so wait_group<NS-1> at iteration
+// i = j + NS - 1 completes both the prefetched B of k-block j and its A.
+__device__ __forceinline__ void conv_tc_mainloop_cpasync(const RunArgs &a, const OpDesc &d, const ConvTile &ct,
+                                                         uint8_t *smem, CtaShared &sh, PipeState &ps) {
+  const int tid = threadIdx.x;
+  const int m0 = ct.m0, n0 = ct.n0, kb0 = ct.kb0, nk = ct.nk;
   const bf16 *X = in_ptr<bf16>(a, d);
   const bf16 *Wt = reinterpret_cast<const bf16 *>(d.w);
   const int HoWo = d.Ho * d.Wo;
-  // per-thread im2col rows: r_i = (tid >> 3) + 32 i, 16-byte chunk c = tid & 7 of the K-block
   const int c = tid & 7;
   int pbase[4], hb[4], wb[4];
   bool rv[4];
@@ -381,10 +464,6 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
   const uint32_t tmem = sh.tmem_base;
   const uint32_t bar_empty0 = smem_u32(&sh.bar_empty[0]);
   const uint32_t bar_accf = smem_u32(&sh.bar_accf);
-
-  // commit groups: MT_STAGES B-prefetch groups (conv_tc_prefetch) precede the loop's groups;
-  // group NS + j holds A (and, for j >= NS, B) of k-block j, so wait_group<NS-1> at iteration
-  // i = j + NS - 1 completes both the prefetched B of k-block j and its A.
   for (int i = 0; i < nk + MT_STAGES - 1; ++i) {
     if (i < nk) {
       const uint32_t f = ps.fill + i;
@@ -433,7 +512,117 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
     }
   }
   cp_async_wait<0>();
-  ps.fill += nk;
+}
+
+__device__ __forceinline__ void conv_epilogue_vals(const RunArgs &a, const OpDesc &d, const CtaShared &sh,
+                                                   int m, int n0, int col, float *v) {
+  const int n = n0 + col;
+  const int nvalid = min(8, d.Co - n);
+  float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (d.flags & OPF_RES) {
+    const bf16 *rp = reinterpret_cast<const bf16 *>(d.res) + (int64_t)m * d.res_cs + d.res_co + n;
+    if (nvalid == 8) ld8_cg(rp, r);
+    else
+      for (int e = 0; e < nvalid; ++e) r[e] = ld1_cg(rp + e);
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) v[e] = act_f(fmaf(v[e], sh.esc[col + e], sh.esh[col + e]) + r[e], d.act);
+  store_out8<bf16>(a, d, m, n, v, nvalid);
+}
+
+// split-K reduce tile (tmn, rc): waits for the S partials of (M,N) tile tmn, sums columns
+// [rc*32, rc*32+32) of its valid rows in split order 0..S-1 (float4 over 4 rows), stages the sums
+// in shared memory and runs the fused epilogue.  The last of the rc reduce tiles resets the
+// arrival counter (S compute + rc reduce arrivals) for the next run.
+__device__ void conv_reduce_tile(const RunArgs &a, const OpDesc &d, int rtile, uint8_t *smem, CtaShared &sh,
+                                 bool wait_splits) {
+  const int tid = threadIdx.x;
+  const int S = d.splits;
+  const int tmn = rtile / d.rc, rc = rtile - (rtile / d.rc) * d.rc;
+  const ConvTile ct = conv_tile_coords(d, tmn * S);
+  int *cnt = a.splitcnt + d.cnt_off + tmn;
+  if (tid == 0) {
+    if (wait_splits) {
+      const unsigned long long t0 = gtimer();
+      unsigned spins = 0;
+      while (ld_acquire(cnt) < S) {
+        if ((++spins & 255) == 0 && gtimer() - t0 > a.timeout_ns) { atomicExch(&a.ctl->error, 3u); break; }
+        __nanosleep(20);
+      }
+    }
+  }
+  // valid accumulator rows form a prefix of the 128 TMEM lanes
+  int nv;
+  if (d.tma) nv = min(d.blk_rows, d.Ho - ct.ho0) * d.Wo;
+  else nv = min(MT_BM, d.M - ct.m0);
+  const int c0 = rc * 32;
+  const int ncol = min(32, d.bn - c0);
+  if (tid < ncol) {
+    const int n = ct.n0 + c0 + tid;
+    sh.esc[c0 + tid] = n < d.Co ? __ldg(reinterpret_cast<const float *>(d.scale) + n) : 0.f;
+    sh.esh[c0 + tid] = n < d.Co ? __ldg(reinterpret_cast<const float *>(d.shift) + n) : 0.f;
+  }
+  __syncthreads();
+  const int nv4 = (nv + 3) >> 2;
+  const float *ws = reinterpret_cast<const float *>(d.ws);
+  float *red = reinterpret_cast<float *>(smem);   // [32 cols][128 rows]
+  const int64_t sstride = (int64_t)d.bn * MT_BM;
+  for (int it = tid; it < ncol * nv4; it += MT_NTHREADS) {
+    const int col = it / nv4, r4 = it - col * nv4;
+    const float4 *p = reinterpret_cast<const float4 *>(ws + ((int64_t)tmn * S * d.bn + c0 + col) * MT_BM) + r4;
+    float4 acc = __ldcg(p);
+    int s2 = 1;
+    for (; s2 + 3 < S; s2 += 4) {
+      const float4 p1 = __ldcg(p + (s2 * sstride) / 4), p2 = __ldcg(p + ((s2 + 1) * sstride) / 4);
+      const float4 p3 = __ldcg(p + ((s2 + 2) * sstride) / 4), p4 = __ldcg(p + ((s2 + 3) * sstride) / 4);
+      acc.x = (((acc.x + p1.x) + p2.x) + p3.x) + p4.x;
+      acc.y = (((acc.y + p1.y) + p2.y) + p3.y) + p4.y;
+      acc.z = (((acc.z + p1.z) + p2.z) + p3.z) + p4.z;
+      acc.w = (((acc.w + p1.w) + p2.w) + p3.w) + p4.w;
+    }
+    for (; s2 < S; ++s2) {
+      const float4 p1 = __ldcg(p + (s2 * sstride) / 4);
+      acc.x += p1.x; acc.y += p1.y; acc.z += p1.z; acc.w += p1.w;
+    }
+    reinterpret_cast<float4 *>(red + col * MT_BM)[r4] = acc;
+  }
+  __syncthreads();
+  for (int it = tid; it < nv * (ncol / 8); it += MT_NTHREADS) {
+    const int r = it % nv, ch = it / nv;
+    const int m = conv_row_pixel(d, ct, r);
+    const int col = c0 + ch * 8;
+    if (m >= 0 && ct.n0 + col < d.Co) {
+      float v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = red[(ch * 8 + e) * MT_BM + r];
+      conv_epilogue_vals(a, d, sh, m, ct.n0, col, v);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int old = atomicAdd(cnt, 1);
+    if (old == S + d.rc - 1) atomicExch(cnt, 0);   // every arrival of this run is in
+  }
+}
+
+__device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_t *smem,
+                             CtaShared &sh, PipeState &ps) {
+  if (d.splits > 1 && tile >= d.tiles_m * d.tiles_n * d.splits) {
+    conv_reduce_tile(a, d, tile - d.tiles_m * d.tiles_n * d.splits, smem, sh, true);
+    return;
+  }
+  const int tid = threadIdx.x;
+  const int S = d.splits;
+  const ConvTile ct = conv_tile_coords(d, tile);
+  const int tmn = ct.tmn, ks = ct.ks, n0 = ct.n0;
+  const uint32_t bar_accf = smem_u32(&sh.bar_accf);
+  if (d.tma) {
+    conv_tc_mainloop_tma(d, ct, smem, sh, ps);
+    for (int i = 0; i < ct.nk; ++i) ps.fullph ^= 1u << ((ps.fill + i) % MT_STAGES);
+  } else {
+    conv_tc_mainloop_cpasync(a, d, ct, smem, sh, ps);
+  }
+  ps.fill += ct.nk;
   mbar_wait(bar_accf, ps.acc_phase);
   ps.acc_phase ^= 1;
   tc_fence_after();
@@ -443,48 +632,30 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
   const int warp = tid >> 5, lane = tid & 31;
   const int q = warp & 3, half = warp >> 2;
   const int r = 32 * q + lane;
-  const int m = m0 + r;
+  const int m = conv_row_pixel(d, ct, r);
   const int hcols = d.bn >> 1;
-  const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+  const uint32_t tl = sh.tmem_base + ((uint32_t)(32 * q) << 16);
   if (S == 1) {
     for (int col = half * hcols; col < (half + 1) * hcols; col += 8) {
       float v[8];
       tmem_ld8(tl + col, v);
-      if (m < d.M && n0 + col < d.Co) conv_epilogue_vals(a, d, sh, m, n0, col, v);
+      if (m >= 0 && n0 + col < d.Co) conv_epilogue_vals(a, d, sh, m, n0, col, v);
     }
   } else {
+    // split-K part: fp32 partial tile -> workspace [tmn*S + ks][bn][128] (valid rows/cols only);
+    // the reduce tiles of this (M,N) tile sum the S partials in split order (deterministic)
     float *ws = reinterpret_cast<float *>(d.ws);
     for (int col = half * hcols; col < (half + 1) * hcols; col += 8) {
       float v[8];
       tmem_ld8(tl + col, v);
       float *p = ws + ((int64_t)(tmn * S + ks) * d.bn + col) * MT_BM + r;
-      if (m < d.M && n0 + col < d.Co)
+      if (m >= 0 && n0 + col < d.Co)
 #pragma unroll
         for (int e = 0; e < 8; ++e) __stcg(p + e * MT_BM, v[e]);
     }
     tc_fence_before();
     __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      const int old = atomicAdd(a.splitcnt + d.cnt_off + tmn, 1);
-      sh.last = (old == S - 1);
-      if (sh.last) {
-        a.splitcnt[d.cnt_off + tmn] = 0;  // ready for the next run
-        __threadfence();
-      }
-    }
-    __syncthreads();
-    if (sh.last && m < d.M) {   // only rows that exist are reduced (M may be << 128 at b=1)
-      for (int col = half * hcols; col < (half + 1) * hcols && n0 + col < d.Co; col += 8) {
-        float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int s2 = 0; s2 < S; ++s2) {  // fixed summation order: deterministic
-          const float *p = ws + ((int64_t)(tmn * S + s2) * d.bn + col) * MT_BM + r;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] += __ldcg(p + e * MT_BM);
-        }
-        if (m < d.M && n0 + col < d.Co) conv_epilogue_vals(a, d, sh, m, n0, col, v);
-      }
-    }
+    if (tid == 0) red_release_add(a.splitcnt + d.cnt_off + tmn, 1);
   }
   tc_fence_before();
   __syncthreads();
@@ -567,7 +738,7 @@ __device__ void conv_simt_tile(const RunArgs &a, const OpDesc &d, int tile, uint
 // a6: depthwise conv (+ folded BN + act); item = (output pixel, 8-channel group)
 // ------------------------------------------------------------------------------------------
 template <typename T, int KH, int KW>
-__device__ __forceinline__ void dw_item(const RunArgs &a, const OpDesc &d, const T *X, const T *Wt,
+__device__ __forceinline__ void dw_item(const RunArgs &a, const OpDesc &d, const T *X, const float *Wt,
                                         int64_t pix, int g) {
   const int n = (int)(pix / (d.Ho * d.Wo));
   const int rem = (int)(pix - (int64_t)n * d.Ho * d.Wo);
@@ -616,15 +787,46 @@ __device__ __forceinline__ void dw_item(const RunArgs &a, const OpDesc &d, const
   store_out8<T>(a, d, pix, g * 8, acc, 8);
 }
 
-// 3x3 depthwise, row-run form: one thread computes RUN consecutive output pixels of one row for
-// one 8-channel group, so the (RUN-1)*S+3 input columns of each kernel row are loaded once and
-// reused by neighbouring outputs; all loads are issued before the arithmetic.  A tile = whole
-// output rows (pix_tile = rows * Wo), item = (row, run segment, channel group), group fastest.
+// packed fp32x2 FMA (sm_100 FFMA2): per lane identical to fmaf, so results are unchanged
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long *>(&a)), "l"(*reinterpret_cast<unsigned long long *>(&b)),
+        "l"(*reinterpret_cast<unsigned long long *>(&c)));
+  return *reinterpret_cast<float2 *>(&r);
+}
+__device__ __forceinline__ void cvt8x2(const Raw8<bf16> &r, float2 *v) {
+  const uint32_t *u = reinterpret_cast<const uint32_t *>(&r.u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = make_float2(__uint_as_float(u[i] << 16), __uint_as_float(u[i] & 0xFFFF0000u));
+}
+__device__ __forceinline__ void cvt8x2(const Raw8<float> &r, float2 *v) {
+  v[0] = make_float2(r.a.x, r.a.y); v[1] = make_float2(r.a.z, r.a.w);
+  v[2] = make_float2(r.b.x, r.b.y); v[3] = make_float2(r.b.z, r.b.w);
+}
+__device__ __forceinline__ Raw8<bf16> ldraw_cg_pred(const bf16 *p, bool ok) {
+  Raw8<bf16> r;
+  r.u = ok ? __ldcg(reinterpret_cast<const uint4 *>(p)) : make_uint4(0, 0, 0, 0);
+  return r;
+}
+__device__ __forceinline__ Raw8<float> ldraw_cg_pred(const float *p, bool ok) {
+  Raw8<float> r;
+  r.a = ok ? __ldcg(reinterpret_cast<const float4 *>(p)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  r.b = ok ? __ldcg(reinterpret_cast<const float4 *>(p) + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+  return r;
+}
+
+// 3x3 depthwise, row-run form: a thread computes RUN consecutive outputs of one row for one
+// 8-channel group; each kernel row's (RUN-1)*S+3 input columns are loaded and converted once and
+// reused by the neighbouring outputs; weights (fp32, [9][C]) stay in registers; packed FFMA2.
+// A tile = whole output rows (pix_tile = rows * Wo); item = (row, run segment, channel group),
+// channel group fastest for coalescing.
 template <typename T, int S, int RUN>
 __device__ void dw3_tile(const RunArgs &a, const OpDesc &d, int tile) {
   constexpr int NC = (RUN - 1) * S + 3;
   const T *X = in_ptr<T>(a, d);
-  const T *Wt = reinterpret_cast<const T *>(d.w);
+  const float *Wt = reinterpret_cast<const float *>(d.w);
   const float *sc = reinterpret_cast<const float *>(d.scale);
   const float *sf = reinterpret_cast<const float *>(d.shift);
   const int cg = d.C >> 3;
@@ -643,45 +845,68 @@ __device__ void dw3_tile(const RunArgs &a, const OpDesc &d, int tile) {
     const int wo0 = seg * RUN;
     const int wi0 = wo0 * S - d.pw;
     const T *xb = X + (int64_t)n * H * W * cs + d.in_co + g * 8;
-    Raw8<T> xr[3][NC];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const int hi = ho * S - d.ph + r;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const int wi = wi0 + c;
-        if (hi >= 0 && hi < H && wi >= 0 && wi < W) ldraw_cg(xb + (int64_t)(hi * W + wi) * cs, xr[r][c]);
-        else zero_raw(xr[r][c]);
-      }
-    }
-    float acc[RUN][8];
+    float2 acc[RUN][4];
 #pragma unroll
     for (int o = 0; o < RUN; ++o)
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc[o][q] = 0.f;
+      for (int q = 0; q < 4; ++q) acc[o][q] = make_float2(0.f, 0.f);
+    Raw8<T> xr[3][NC];
 #pragma unroll
-    for (int r = 0; r < 3; ++r)
+    for (int r = 0; r < 3; ++r) {   // every load of the item issued before any arithmetic
+      const int hi = ho * S - d.ph + r;
+      const bool rok = hi >= 0 && hi < H;
 #pragma unroll
-      for (int s2 = 0; s2 < 3; ++s2) {
-        float w[8];
-        ld8_nc(Wt + (r * 3 + s2) * d.C + g * 8, w);
+      for (int c = 0; c < NC; ++c) {
+        const int wi = wi0 + c;
+        xr[r][c] = ldraw_cg_pred(xb + (int64_t)(hi * W + wi) * cs, rok && wi >= 0 && wi < W);
+      }
+    }
 #pragma unroll
-        for (int o = 0; o < RUN; ++o) {
-          float x[8];
-          cvt8(xr[r][o * S + s2], x);
+    for (int r = 0; r < 3; ++r) {
+      float2 w2[3][4];   // this kernel row's 3 taps (fp32 weights, [9][C])
 #pragma unroll
-          for (int q = 0; q < 8; ++q) acc[o][q] = fmaf(x[q], w[q], acc[o][q]);
+      for (int t = 0; t < 3; ++t) {
+        const float4 lo = __ldg(reinterpret_cast<const float4 *>(Wt + (r * 3 + t) * d.C + g * 8));
+        const float4 hi = __ldg(reinterpret_cast<const float4 *>(Wt + (r * 3 + t) * d.C + g * 8) + 1);
+        w2[t][0] = make_float2(lo.x, lo.y); w2[t][1] = make_float2(lo.z, lo.w);
+        w2[t][2] = make_float2(hi.x, hi.y); w2[t][3] = make_float2(hi.z, hi.w);
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        float2 x[4];
+        cvt8x2(xr[r][c], x);
+#pragma unroll
+        for (int s2 = 0; s2 < 3; ++s2) {
+          // column c feeds output o when o*S + s2 == c
+          if ((c - s2) >= 0 && (c - s2) % S == 0 && (c - s2) / S < RUN) {
+            const int o = (c - s2) / S;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[o][q] = ffma2(x[q], w2[s2][q], acc[o][q]);
+          }
         }
       }
-    float scv[8], sfv[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) { scv[q] = __ldg(sc + g * 8 + q); sfv[q] = __ldg(sf + g * 8 + q); }
+    }
+    float2 sc2[4], sf2[4];
+    {
+      const float4 a0 = __ldg(reinterpret_cast<const float4 *>(sc + g * 8));
+      const float4 a1 = __ldg(reinterpret_cast<const float4 *>(sc + g * 8) + 1);
+      const float4 b0 = __ldg(reinterpret_cast<const float4 *>(sf + g * 8));
+      const float4 b1 = __ldg(reinterpret_cast<const float4 *>(sf + g * 8) + 1);
+      sc2[0] = make_float2(a0.x, a0.y); sc2[1] = make_float2(a0.z, a0.w);
+      sc2[2] = make_float2(a1.x, a1.y); sc2[3] = make_float2(a1.z, a1.w);
+      sf2[0] = make_float2(b0.x, b0.y); sf2[1] = make_float2(b0.z, b0.w);
+      sf2[2] = make_float2(b1.x, b1.y); sf2[3] = make_float2(b1.z, b1.w);
+    }
 #pragma unroll
     for (int o = 0; o < RUN; ++o) {
       if (wo0 + o < d.Wo) {
         float y[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) y[q] = act_f(fmaf(acc[o][q], scv[q], sfv[q]), d.act);
+        for (int q = 0; q < 4; ++q) {
+          const float2 t = ffma2(acc[o][q], sc2[q], sf2[q]);
+          y[2 * q] = act_f(t.x, d.act);
+          y[2 * q + 1] = act_f(t.y, d.act);
+        }
         store_out8<T>(a, d, (int64_t)gr * d.Wo + wo0 + o, g * 8, y, 8);
       }
     }
@@ -696,7 +921,7 @@ __device__ void dw_tile(const RunArgs &a, const OpDesc &d, int tile) {
     return;
   }
   const T *X = in_ptr<T>(a, d);
-  const T *Wt = reinterpret_cast<const T *>(d.w);
+  const float *Wt = reinterpret_cast<const float *>(d.w);
   const int cg = d.C >> 3;
   const int p0 = tile * d.pix_tile;
   const int np = min(d.pix_tile, d.N * d.Ho * d.Wo - p0);
@@ -976,7 +1201,19 @@ __device__ void run_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_t *s
 __device__ __forceinline__ void tile_out_range(const OpDesc &d, int tile, int64_t &p0, int64_t &p1) {
   const int64_t npix = (int64_t)d.N * d.Ho * d.Wo;
   switch (d.tk) {
-    case TK_CONV_TC: p0 = (int64_t)((tile / d.splits) / d.tiles_n) * MT_BM; p1 = p0 + MT_BM; break;
+    case TK_CONV_TC:
+      if (d.splits > 1 && tile >= d.tiles_m * d.tiles_n * d.splits)   // reduce tile -> its (M,N) tile
+        tile = ((tile - d.tiles_m * d.tiles_n * d.splits) / d.rc) * d.splits;
+      if (d.tma) {
+        const int mt = (tile / d.splits) / d.tiles_n, img = mt / d.blk_tpi;
+        const int ho0 = (mt - img * d.blk_tpi) * d.blk_rows;
+        p0 = ((int64_t)img * d.Ho + ho0) * d.Wo;
+        p1 = ((int64_t)img * d.Ho + min(d.Ho, ho0 + d.blk_rows)) * d.Wo;
+      } else {
+        p0 = (int64_t)((tile / d.splits) / d.tiles_n) * MT_BM;
+        p1 = p0 + MT_BM;
+      }
+      break;
     case TK_CONV_SIMT: p0 = (int64_t)(tile / d.tiles_n) * MT_SIMT_BM; p1 = p0 + MT_SIMT_BM; break;
     case TK_GAP: p0 = tile / ((d.Co / 8 + 31) / 32); p1 = p0 + 1; break;
     case TK_FC: p0 = (int64_t)(tile / ((d.Co + MT_FC_ROWS - 1) / MT_FC_ROWS)) * MT_FC_BATCH; p1 = p0 + MT_FC_BATCH; break;
@@ -1001,7 +1238,11 @@ __device__ __forceinline__ void tile_in_range(const OpDesc &d, int64_t p0, int64
 // completion block a finished tile contributes to (-1: none, e.g. a non-final split-K part)
 __device__ __forceinline__ int tile_block(const OpDesc &d, int tile, const CtaShared &sh) {
   switch (d.tk) {
-    case TK_CONV_TC: return (d.splits == 1 || sh.last) ? (tile / d.splits) / d.tiles_n : -1;
+    case TK_CONV_TC: {
+      if (d.splits == 1) return tile / d.tiles_n;
+      const int nct = d.tiles_m * d.tiles_n * d.splits;
+      return tile >= nct ? ((tile - nct) / d.rc) / d.tiles_n : -1;   // only reduce tiles complete
+    }
     case TK_CONV_SIMT: return tile / d.tiles_n;
     case TK_GAP: return tile / ((d.Co / 8 + 31) / 32);
     case TK_FC: return tile / ((d.Co + MT_FC_ROWS - 1) / MT_FC_ROWS);
@@ -1012,6 +1253,7 @@ __device__ __forceinline__ int tile_block(const OpDesc &d, int tile, const CtaSh
 // work that needs no producer data: issued before the dependency wait so it overlaps it
 __device__ void tile_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaShared &sh, const PipeState &ps) {
   if (d.tk == TK_CONV_TC) {
+    if (d.splits > 1 && tile >= d.tiles_m * d.tiles_n * d.splits) return;   // reduce tile
     conv_tc_prefetch(d, tile, smem, sh, ps);
   } else if (d.tk == TK_FC) {
     const int rb = (int)(tile % ((d.Co + MT_FC_ROWS - 1) / MT_FC_ROWS));
@@ -1040,7 +1282,10 @@ __device__ __forceinline__ uint8_t *smem_base() {
 __device__ void cta_setup(CtaShared &sh, bool need_tmem) {
   const int tid = threadIdx.x;
   if (tid == 0) {
-    for (int s = 0; s < MT_STAGES; ++s) mbar_init(smem_u32(&sh.bar_empty[s]), 1);
+    for (int s = 0; s < MT_STAGES; ++s) {
+      mbar_init(smem_u32(&sh.bar_empty[s]), 1);
+      mbar_init(smem_u32(&sh.bar_full[s]), 1);
+    }
     mbar_init(smem_u32(&sh.bar_accf), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1177,11 +1422,29 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
           continue;
         }
         int64_t lo = INT64_MAX, hi = 0;
-        if (d.dep_kind[k] & 1) { lo = i0; hi = i1; }
-        if (d.dep_kind[k] & 2) { lo = min(lo, p0); hi = max(hi, p1); }
-        const int pb = __ldg(&pd->pix_blk), need = __ldg(&pd->blk_need), off = __ldg(&pd->blk_off);
-        const int nbk = __ldg(&pd->nblk);
-        const int b0 = (int)(lo / pb), b1 = min(nbk - 1, (int)((hi - 1) / pb));
+        bool need_in = true, need_res = true;
+        if (d.tk == TK_CONV_TC && d.splits > 1) {
+          const bool red_tile = sh.tile >= d.tiles_m * d.tiles_n * d.splits;
+          need_in = !red_tile;   // compute parts read the input only,
+          need_res = red_tile;   // reduce tiles (epilogue) the residual only
+        }
+        if ((d.dep_kind[k] & 1) && need_in) { lo = i0; hi = i1; }
+        if ((d.dep_kind[k] & 2) && need_res) { lo = min(lo, p0); hi = max(hi, p1); }
+        if (hi <= lo) continue;
+        const int need = __ldg(&pd->blk_need), off = __ldg(&pd->blk_off), nbk = __ldg(&pd->nblk);
+        int b0, b1;
+        const int br = __ldg(&pd->blk_rows);
+        if (br > 0) {   // producer blocks are whole-row M tiles: block = n * tpi + ho / rows
+          const int pWo = __ldg(&pd->Wo), pHoWo = __ldg(&pd->Ho) * pWo, tpi = __ldg(&pd->blk_tpi);
+          const int na = (int)(lo / pHoWo), nb2 = (int)((hi - 1) / pHoWo);
+          b0 = na * tpi + (int)((lo - (int64_t)na * pHoWo) / pWo) / br;
+          b1 = nb2 * tpi + (int)((hi - 1 - (int64_t)nb2 * pHoWo) / pWo) / br;
+        } else {
+          const int pb = __ldg(&pd->pix_blk);
+          b0 = (int)(lo / pb);
+          b1 = (int)((hi - 1) / pb);
+        }
+        b1 = min(nbk - 1, b1);
         for (int b = b0; b <= b1 && ok; ++b) {
           while (ld_acquire(a.blkcnt + off + b) < need) {
             if ((++spins & 255) == 0) {
@@ -1212,7 +1475,7 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
 __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
   uint8_t *smem = smem_base();
   __shared__ __align__(16) CtaShared sh;
-  PipeState ps{0u, 0u};
+  PipeState ps{0u, 0u, 0u};
   if (threadIdx.x < 64) sh.complete[threadIdx.x] = 0u;
   cta_setup(sh, true);
   bool ok = grid_barrier(a, sh);
@@ -1251,7 +1514,7 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
 __global__ void __launch_bounds__(MT_NTHREADS, 1) op_kernel(RunArgs a, int op) {
   uint8_t *smem = smem_base();
   __shared__ __align__(16) CtaShared sh;
-  PipeState ps{0u, 0u};
+  PipeState ps{0u, 0u, 0u};
   load_desc(sh, a.ops + op);
   const bool tc = __ldg(&a.ops[op].tk) == TK_CONV_TC;
   cta_setup(sh, tc);
@@ -1259,6 +1522,7 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) op_kernel(RunArgs a, int op) {
     if (threadIdx.x == 0) { sh.t_pick = gtimer(); sh.t_mma = 0; sh.home = -1; }
     tile_prefetch(sh.d, t, smem, sh, ps);
     if (threadIdx.x == 0) sh.t_deps = gtimer();
+    __syncthreads();
     run_tile(a, sh.d, t, smem, sh, ps);
     if (threadIdx.x == 0) trace_tile(a, sh, op, t);
   }
@@ -1271,13 +1535,14 @@ __global__ void __launch_bounds__(MT_NTHREADS) op_kernel_small(RunArgs a, int op
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(16) CtaShared sh;
-  PipeState ps{0u, 0u};
+  PipeState ps{0u, 0u, 0u};
   load_desc(sh, a.ops + op);
   __syncthreads();
   for (int t = blockIdx.x; t < sh.d.tiles; t += gridDim.x) {
     if (threadIdx.x == 0) { sh.t_pick = gtimer(); sh.t_mma = 0; sh.home = -1; }
     tile_prefetch(sh.d, t, smem, sh, ps);
     if (threadIdx.x == 0) sh.t_deps = gtimer();
+    __syncthreads();
     run_tile(a, sh.d, t, smem, sh, ps);
     if (threadIdx.x == 0) trace_tile(a, sh, op, t);
   }
@@ -1309,13 +1574,25 @@ __global__ void weight_pack_kernel(int mode, const float *src, void *dst, OpDesc
       if (mode == 1) reinterpret_cast<bf16 *>(dst)[i] = __float2bfloat16_rn(v);
       else reinterpret_cast<float *>(dst)[i] = v;
     }
+  } else if (mode == 5) {  // conv for the TMA mainloop: K = (tap, 64-channel blocks), zero padded
+    const int rows = d.tiles_n * d.bn;
+    const int ld = d.Kpad, per_tap = d.cblks * 64;
+    const int64_t total = (int64_t)rows * ld;
+    for (int64_t i = tid; i < total; i += stride) {
+      const int row = (int)(i / ld), k = (int)(i - (int64_t)row * ld);
+      const int tap = k / per_tap, ci = k - tap * per_tap;
+      const int r = tap / d.kw, s2 = tap - r * d.kw;
+      float v = 0.f;
+      if (row < d.Co && ci < cin_real) v = src[(((int64_t)row * cin_real + ci) * d.kh + r) * d.kw + s2];
+      reinterpret_cast<bf16 *>(dst)[i] = __float2bfloat16_rn(v);
+    }
   } else if (mode == 3) {  // depthwise [C][1][kh][kw] -> [kh*kw][C]
     const int64_t total = (int64_t)d.kh * d.kw * d.C;
     for (int64_t i = tid; i < total; i += stride) {
       const int tap = (int)(i / d.C), ch = (int)(i - (int64_t)tap * d.C);
       const float v = src[(int64_t)ch * d.kh * d.kw + tap];
-      if (d.prec == 0) reinterpret_cast<bf16 *>(dst)[i] = __float2bfloat16_rn(v);
-      else reinterpret_cast<float *>(dst)[i] = v;
+      // bf16 graphs: the weight value is rounded to bf16 (as every conv weight), stored as fp32
+      reinterpret_cast<float *>(dst)[i] = d.prec == 0 ? __bfloat162float(__float2bfloat16_rn(v)) : v;
     }
   } else if (mode == 4) {  // FC [out][C*H*W] (NCHW flatten) -> [out][H*W*C] (NHWC flatten)
     const int64_t total = (int64_t)d.Co * d.K;

@@ -49,12 +49,21 @@ struct OpDesc {
   // pix_blk; block b of this op is complete when blkcnt[blk_off + b] == blk_need
   int32_t pix_blk, blk_need, nblk, blk_off;
   int32_t pix_tile;                 // pointwise tiles: output pixels per tile
-  int32_t pad1;
+  int32_t blk_rows;                 // >0: blocks are whole-row M-tiles (TMA conv): block of pixel p =
+                                    //     n * blk_tpi + ho / blk_rows
+  int32_t blk_tpi;                  // tiles (blocks) per image for blk_rows > 0
+  int32_t tma;                      // 1: TMA mainloop (whole-row M tiles, K-block = tap x 64 ch)
+  int32_t cblks;                    // TMA: 64-channel blocks per tap
+  int32_t a_bytes;                  // TMA: bytes of one A box (rows * Wo * 128)
+  int32_t rc;                       // split-K: reduce tiles per (M,N) tile (32 columns each); the op's
+                                    // tiles are [tmn*splits compute tiles][tmn*rc reduce tiles]
+  int32_t pad3;
   int32_t M, K, Kpad, nkb;          // GEMM view (conv / FC)
   int32_t bn, tiles_m, tiles_n, splits;
   int32_t kb_per_split, tiles, cnt_off, pad0;
   uint64_t in, res, out, w, scale, shift, ws;   // device addresses (filled at bind)
   uint64_t ins[MT_MAXIN];                        // ADD inputs
+  uint64_t tmap_a, tmap_b;                       // TMA: device addresses of CUtensorMaps
 };
 
 // Device-side control block in the workspace (counters are zero between runs).

@@ -107,6 +107,26 @@ __global__ void k_gridbar(unsigned *cnt, unsigned *gen, unsigned long long *out,
   if (threadIdx.x == 0 && blockIdx.x == 0) out[10] = (c1 - c0) / iters;
 }
 
+// ---- single-CTA L2 read pattern: each thread issues NL independent 16-byte ld.global.cg loads ----
+template <int NL>
+__global__ void k_l2read(const uint4 *src, unsigned long long *out, int stride_elems) {
+  const int t = threadIdx.x;
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  long long c0 = clock64();
+  uint4 v[NL];
+#pragma unroll
+  for (int i = 0; i < NL; ++i)
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v[i].x), "=r"(v[i].y), "=r"(v[i].z), "=r"(v[i].w)
+                 : "l"(src + (size_t)i * stride_elems + t));
+#pragma unroll
+  for (int i = 0; i < NL; ++i) { acc.x ^= v[i].x; acc.y ^= v[i].y; }
+  __syncthreads();
+  long long c1 = clock64();
+  if (t == 0) out[blockIdx.x] = c1 - c0;
+  if (acc.x == 0x12345 && acc.y == 7) out[100] = 1;
+}
+
 int main() {
   int *buf, *flag;
   unsigned *cnt;
@@ -130,9 +150,28 @@ int main() {
     cudaLaunchCooperativeKernel((void *)k_gridbar, 148, 256, a2, 0, 0);
     cudaDeviceSynchronize();
   }
+  {
+    uint4 *big;
+    cudaMalloc(&big, 64 << 20);
+    cudaMemset(big, 1, 64 << 20);
+    for (int rep = 0; rep < 2; ++rep) {
+      k_l2read<1><<<1, 256>>>(big, out, 256);
+      cudaDeviceSynchronize();
+      unsigned long long c1 = out[0];
+      k_l2read<18><<<1, 256>>>(big, out, 256);
+      cudaDeviceSynchronize();
+      unsigned long long c18 = out[0];
+      k_l2read<18><<<148, 256>>>(big, out, 256);
+      cudaDeviceSynchronize();
+      unsigned long long c18all = out[0];
+      printf("1 CTA x 256 thr: 1 load/thr %llu cyc (4 KB); 18 loads/thr %llu cyc (72 KB -> %.1f B/cyc); 148 CTAs same data: %llu cyc\n",
+             c1, c18, 73728.0 / c18, c18all);
+    }
+  }
   printf("L2 hit (ld.cg) %llu cyc | atomicAdd RTT %llu | red.release %llu | st+red.release %llu | ld.acquire %llu | threadfence %llu\n",
          out[0], out[1], out[2], out[3], out[4], out[5]);
   printf("globaltimer min step %llu ns | SM clock ~%llu MHz | __syncthreads(256) %llu cyc | grid barrier(148) %llu cyc\n",
          out[6], out[7] / 100, out[9], out[10]);
   return 0;
 }
+
