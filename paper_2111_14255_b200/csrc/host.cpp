@@ -381,7 +381,7 @@ static mt_status plan_graphs(mt_ctx *c) {
           } else if (bf16) {
             d.tk = TK_CONV_TC;
             d.M = g.batch * os.h * os.w;
-            d.bn = os.c <= 16 ? 16 : os.c <= 32 ? 32 : os.c <= 64 ? 64 : 128;
+            d.bn = os.c <= 16 ? 16 : os.c <= 32 ? 32 : os.c <= 64 ? 64 : 128;   // refined below
             d.tiles_n = (int)cdiv(os.c, d.bn);
             // TMA mainloop: whole output rows per M tile; a K-block is one tap x 64 channels, loaded
             // as one 4-D box {64 ch, Wo*sw, R*sh, 1} with element strides {1, sw, sh, 1}
@@ -403,12 +403,31 @@ static mt_status plan_graphs(mt_ctx *c) {
               d.nkb = d.Kpad / MT_BK;
               d.tiles_m = (int)cdiv(d.M, MT_BM);
             }
-            const int tmn = d.tiles_m * d.tiles_n;
-            int splits = 1;
-            if (tmn < 74 && d.nkb >= 8) {
-              splits = (int)std::min<int64_t>(std::min<int64_t>(cdiv(148, tmn), d.nkb / 4), 12);
-              splits = std::max(splits, 1);
+            // (bn, splits) from a latency model of one op at b=1..8 (shape-only, so outputs are
+            // schedule-invariant): waves x tile time (+ a reduce hop when split), with ~74 SMs
+            // available to the op (two tenants sharing the GPU).  Per-k-block and epilogue costs are
+            // the measured executor-trace figures.
+            int best_bn = d.bn, splits = 1;
+            {
+              double best = 1e30;
+              const int bn_max = d.bn;
+              for (int bn = bn_max; bn >= 32 || bn == bn_max; bn >>= 1) {
+                const int64_t tn = cdiv(os.c, bn), tmn_c = (int64_t)d.tiles_m * tn;
+                const double t_kb = 0.09 + 0.0006 * bn, t_epi = 0.5 + 0.02 * bn;
+                for (int sp = 1; sp <= 12; ++sp) {
+                  if (sp > 1 && d.nkb / sp < 4) break;
+                  const int64_t kbps = cdiv(d.nkb, sp);
+                  const int64_t waves = cdiv(tmn_c * sp, 74);
+                  double t = waves * (0.8 + kbps * t_kb + (sp == 1 ? t_epi : 0.4));
+                  if (sp > 1) t += 2.0 + cdiv(tmn_c * std::max(1, bn / 32), 74) * (0.8 + 0.04 * sp * bn / 32.0);
+                  if (t < best * 0.97) { best = t; best_bn = bn; splits = sp; }
+                }
+                if (bn <= 32) break;
+              }
             }
+            d.bn = best_bn;
+            d.tiles_n = (int)cdiv(os.c, d.bn);
+            const int tmn = d.tiles_m * d.tiles_n;
             d.kb_per_split = (int)cdiv(d.nkb, splits);
             d.splits = (int)cdiv(d.nkb, d.kb_per_split);
             d.rc = d.splits > 1 ? std::max(1, d.bn / 32) : 0;

@@ -160,6 +160,22 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float *v) {
   v[3] = __uint_as_float(r3); v[4] = __uint_as_float(r4); v[5] = __uint_as_float(r5);
   v[6] = __uint_as_float(r6); v[7] = __uint_as_float(r7);
 }
+// 32 lanes x 32 bit x 32 columns in one load (one wait for 32 accumulator columns)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
 // UMMA shared-memory descriptor: K-major operand, 128-byte swizzle, 8-row atoms of 1024 B
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   uint64_t d = 0;
@@ -636,22 +652,69 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
   const int hcols = d.bn >> 1;
   const uint32_t tl = sh.tmem_base + ((uint32_t)(32 * q) << 16);
   if (S == 1) {
-    for (int col = half * hcols; col < (half + 1) * hcols; col += 8) {
-      float v[8];
-      tmem_ld8(tl + col, v);
-      if (m >= 0 && n0 + col < d.Co) conv_epilogue_vals(a, d, sh, m, n0, col, v);
+    if (hcols >= 32) {
+      for (int cb = half * hcols; cb < (half + 1) * hcols; cb += 32) {
+        // residual of these 32 columns requested before the TMEM drain (hides its L2 latency)
+        uint4 rr[4] = {};
+        const bool okrow = m >= 0;
+        if ((d.flags & OPF_RES) && okrow && n0 + cb + 32 <= d.Co) {
+          const bf16 *rp = reinterpret_cast<const bf16 *>(d.res) + (int64_t)m * d.res_cs + d.res_co + n0 + cb;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) rr[j] = __ldcg(reinterpret_cast<const uint4 *>(rp) + j);
+        }
+        float v[32];
+        tmem_ld32(tl + cb, v);
+        if (okrow) {
+          if ((d.flags & OPF_RES) && n0 + cb + 32 <= d.Co) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float rf[8];
+              Raw8<bf16> raw;
+              raw.u = rr[j];
+              cvt8(raw, rf);
+              float y[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                y[e] = act_f(fmaf(v[j * 8 + e], sh.esc[cb + j * 8 + e], sh.esh[cb + j * 8 + e]) + rf[e], d.act);
+              store_out8<bf16>(a, d, m, n0 + cb + j * 8, y, 8);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (n0 + cb + j * 8 < d.Co) conv_epilogue_vals(a, d, sh, m, n0, cb + j * 8, v + j * 8);
+          }
+        }
+      }
+    } else {
+      for (int col = half * hcols; col < (half + 1) * hcols; col += 8) {
+        float v[8];
+        tmem_ld8(tl + col, v);
+        if (m >= 0 && n0 + col < d.Co) conv_epilogue_vals(a, d, sh, m, n0, col, v);
+      }
     }
   } else {
     // split-K part: fp32 partial tile -> workspace [tmn*S + ks][bn][128] (valid rows/cols only);
     // the reduce tiles of this (M,N) tile sum the S partials in split order (deterministic)
     float *ws = reinterpret_cast<float *>(d.ws);
-    for (int col = half * hcols; col < (half + 1) * hcols; col += 8) {
-      float v[8];
-      tmem_ld8(tl + col, v);
-      float *p = ws + ((int64_t)(tmn * S + ks) * d.bn + col) * MT_BM + r;
-      if (m >= 0 && n0 + col < d.Co)
+    if (hcols >= 32) {
+      for (int cb = half * hcols; cb < (half + 1) * hcols; cb += 32) {
+        float v[32];
+        tmem_ld32(tl + cb, v);
+        float *p = ws + ((int64_t)(tmn * S + ks) * d.bn + cb) * MT_BM + r;
+        if (m >= 0)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) __stcg(p + e * MT_BM, v[e]);
+          for (int e = 0; e < 32; ++e)
+            if (n0 + cb + e < d.Co) __stcg(p + e * MT_BM, v[e]);
+      }
+    } else {
+      for (int col = half * hcols; col < (half + 1) * hcols; col += 8) {
+        float v[8];
+        tmem_ld8(tl + col, v);
+        float *p = ws + ((int64_t)(tmn * S + ks) * d.bn + col) * MT_BM + r;
+        if (m >= 0 && n0 + col < d.Co)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) __stcg(p + e * MT_BM, v[e]);
+      }
     }
     tc_fence_before();
     __syncthreads();
