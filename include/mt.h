@@ -113,8 +113,9 @@ typedef struct {
 
 /* options for mt_set_option */
 typedef enum {
-  MT_OPT_STEAL = 1,        /* 1 (default): CTAs help other tenants when their own queue is */
-                           /* empty or blocked; 0: strict per-tenant SM partition          */
+  MT_OPT_STEAL = 1,        /* 0: strict per-tenant SM partition; 1: when its home tenant's  */
+                           /* slice is fully claimed a CTA helps the others, round-robin;   */
+                           /* 2 (default): ... the tenant with most unclaimed ops first     */
   MT_OPT_NUM_SMS = 2,      /* host-only contexts: SM count used for the partition (148)    */
   MT_OPT_TIMEOUT_MS = 3,   /* device spin timeout (default 2000 ms)                         */
   MT_OPT_CTAS_PER_SM = 4   /* reserved (1)                                                  */
@@ -211,10 +212,12 @@ mt_status mt_profile_batch_pointers(mt_ctx *ctx, int32_t n_cand, const int32_t *
 mt_status mt_get_activation(mt_ctx *ctx, int32_t tenant, int32_t op, void *host_dst,
                             size_t bytes);
 
-/* Debug tracing: when enabled, every executed tile appends one record of 8 uint64 to
+/* Debug tracing: when enabled, every executed tile appends one record of 16 uint64 to
  * the caller's DEVICE buffer: [0] op | tile << 32 (global op id), [1] smid | cta << 32,
  * [2] claim time, [3] dependencies satisfied, [4] tensor-core mainloop done (0 if none),
- * [5] tile end, [6] home tenant of the CTA (-1 in baselines), [7] 0; times are %globaltimer ns.
+ * [5] tile end (after the release), [6] home tenant of the CTA (-1 in baselines), [7] tile body
+ * done (before the release), [8] first pipeline stage landed, [9] last MMA issued, [10] last
+ * A box issued (TMA convs; else 0), [11..15] 0; times are %globaltimer ns.
  * capacity = records; 0 / NULL disables.  Resets the record counter. */
 mt_status mt_set_trace(mt_ctx *ctx, void *dev_buf, int64_t capacity);
 mt_status mt_trace_count(mt_ctx *ctx, int64_t *n_records);

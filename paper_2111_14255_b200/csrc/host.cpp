@@ -25,7 +25,7 @@ struct mt_ctx {
   bool host_only = true;
   int n_sms = 148;
   int grid = 148;
-  int steal = 1;
+  int steal = 2;
   int64_t timeout_ms = 2000;
   bool loaded = false, bound = false, has_sched = false;
   std::vector<Tenant> T;
@@ -431,6 +431,15 @@ static mt_status plan_graphs(mt_ctx *c) {
             d.kb_per_split = (int)cdiv(d.nkb, splits);
             d.splits = (int)cdiv(d.nkb, d.kb_per_split);
             d.rc = d.splits > 1 ? std::max(1, d.bn / 32) : 0;
+            if (d.tma) {   // pipeline depth from the real box sizes (SW128 needs 1 KB alignment)
+              d.st_boff = (int)rup(d.a_bytes, 1024);
+              d.st_bytes = d.st_boff + (int)rup(d.bn * 128, 1024);
+              d.nst = std::min(MT_MAXST, MT_PIPE_BYTES / d.st_bytes);
+            } else {
+              d.st_boff = 16 * 1024;
+              d.st_bytes = 32 * 1024;
+              d.nst = MT_STAGES;
+            }
             d.tiles = tmn * d.splits + tmn * d.rc;
             wp.mode = d.tma ? 5 : 1;
             wp.bytes = (int64_t)d.tiles_n * d.bn * d.Kpad * 2;
@@ -806,7 +815,10 @@ mt_status mt_destroy(mt_ctx *c) {
 mt_status mt_set_option(mt_ctx *c, int32_t option, int64_t value) {
   if (!c) return MT_ERR_ARG;
   switch (option) {
-    case MT_OPT_STEAL: c->steal = value ? 1 : 0; return MT_OK;
+    case MT_OPT_STEAL:
+      if (value < 0 || value > 2) return fail(c, MT_ERR_ARG, "steal must be 0, 1 or 2");
+      c->steal = (int)value;
+      return MT_OK;
     case MT_OPT_NUM_SMS:
       if (!c->host_only) return fail(c, MT_ERR_STATE, "NUM_SMS only settable on host-only contexts");
       if (value < 1 || value > 4096) return fail(c, MT_ERR_ARG, "bad NUM_SMS");

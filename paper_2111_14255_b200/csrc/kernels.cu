@@ -25,18 +25,17 @@ typedef __nv_bfloat16 bf16;
 // ------------------------------------------------------------------------------------------
 // shared-memory map of a CTA (1024-aligned base)
 // ------------------------------------------------------------------------------------------
-static constexpr int A_STAGE = MT_BM * MT_BK * 2;          // 16 KB: 128 rows x 128 B
-static constexpr int B_STAGE = 128 * MT_BK * 2;            // 16 KB: up to BN = 128 rows
-static constexpr int PIPE_BYTES = MT_STAGES * (A_STAGE + B_STAGE);
+static constexpr int PIPE_BYTES = MT_PIPE_BYTES;   // conv pipeline ring (stage geometry per op)
 static constexpr int TMEM_COLS = 128;
 
 struct CtaShared {
-  unsigned long long bar_full[MT_STAGES];    // TMA: stage loaded (expect_tx)
-  unsigned long long bar_empty[MT_STAGES];
+  unsigned long long bar_full[MT_MAXST];     // TMA: stage loaded (expect_tx)
+  unsigned long long bar_empty[MT_MAXST];    // stage consumed by the MMAs (tcgen05.commit)
   unsigned long long bar_accf;
   uint32_t tmem_base;
   int op, tile, last, ok, home, ten;
-  unsigned long long t_pick, t_deps, t_mma, t_run;
+  unsigned long long t_pick, t_deps, t_mma, t_run, t_first, t_lastmma, t_aissue;
+  unsigned long long t_kb[4], t_is[1];
   int cur[MT_MAXT], end[MT_MAXT];
   uint32_t complete[64];      // bitset of ops observed fully complete (global op id < 2048)
   float esc[128], esh[128];   // epilogue scale / shift of the current conv tile's columns
@@ -44,10 +43,12 @@ struct CtaShared {
 };
 static constexpr int SMEM_BYTES = 1024 + PIPE_BYTES;   // + static __shared__ CtaShared
 
+// Every conv tile drains its pipeline (waits for the accumulator), so each tile starts with all
+// stages free; only the mbarrier phase parities persist between tiles.
 struct PipeState {
-  uint32_t fill;       // k-blocks loaded so far by this CTA (stage ring position)
+  uint32_t eph;        // bit s: parity of the next completion of empty[s]
+  uint32_t fph;        // bit s: parity of the next completion of full[s]
   uint32_t acc_phase;  // parity of the accumulator-ready barrier
-  uint32_t fullph;     // bit s: parity of the next phase of the TMA full barrier of stage s
 };
 
 // ------------------------------------------------------------------------------------------
@@ -359,8 +360,12 @@ __device__ __forceinline__ void tma_issue_a(const OpDesc &d, const ConvTile &c, 
   tma_load_4d(dst, d.tmap_a, bar, cb * 64, s - d.pw, c.ho0 * d.sh + r - d.ph, c.img);
 }
 
+// parity helpers: k-block i of a tile uses stage i % nst; its j-th use (j = i / nst) of the stage
+// within the tile completes the stage's barriers with parity (start parity ^ (j & 1))
+__device__ __forceinline__ uint32_t stage_par(uint32_t bits, int s, int j) { return ((bits >> s) & 1u) ^ (uint32_t)(j & 1); }
+
 // Work that needs no producer data, issued BEFORE the tile waits for its dependencies so the weight
-// stream overlaps the wait: the weight (B) tiles of the first min(nk, MT_STAGES) k-blocks and the
+// stream overlaps the wait: the weight (B) tiles of the first min(nk, nst) k-blocks and the
 // epilogue constants.  TMA path: thread 0 arms each stage's full barrier for A+B bytes and issues
 // B; A follows once the producers are complete.  cp.async path: one commit group per k-block.
 __device__ void conv_tc_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaShared &sh,
@@ -368,28 +373,23 @@ __device__ void conv_tc_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaSh
   const int tid = threadIdx.x;
   const ConvTile ct = conv_tile_coords(d, tile);
   const bf16 *Wt = reinterpret_cast<const bf16 *>(d.w);
-  const uint32_t sB = smem_u32(smem) + MT_STAGES * A_STAGE;
-  const uint32_t bar_empty0 = smem_u32(&sh.bar_empty[0]);
+  const uint32_t s0 = smem_u32(smem);
   if (d.tma) {
     if (tid == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(d.tmap_a) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(d.tmap_b) : "memory");
       const uint32_t bar_full0 = smem_u32(&sh.bar_full[0]);
-      for (int i = 0; i < MT_STAGES && i < ct.nk; ++i) {
-        const uint32_t f = ps.fill + i;
-        const int s = f % MT_STAGES;
-        if (f >= MT_STAGES) mbar_wait(bar_empty0 + 8 * s, ((f / MT_STAGES) - 1) & 1);
-        mbar_expect_tx(bar_full0 + 8 * s, (uint32_t)(d.a_bytes + d.bn * 128));
-        tma_load_2d(sB + s * B_STAGE, d.tmap_b, bar_full0 + 8 * s, (ct.kb0 + i) * MT_BK, ct.n0);
+      for (int i = 0; i < d.nst && i < ct.nk; ++i) {
+        mbar_expect_tx(bar_full0 + 8 * i, (uint32_t)(d.a_bytes + d.bn * 128));
+        tma_load_2d(s0 + i * d.st_bytes + d.st_boff, d.tmap_b, bar_full0 + 8 * i, (ct.kb0 + i) * MT_BK, ct.n0);
       }
     }
   } else {
     const int c = tid & 7;
     for (int i = 0; i < MT_STAGES; ++i) {
       if (i < ct.nk) {
-        const uint32_t f = ps.fill + i;
-        const int s = f % MT_STAGES;
-        if (f >= MT_STAGES) mbar_wait(bar_empty0 + 8 * s, ((f / MT_STAGES) - 1) & 1);
         const int kb = ct.kb0 + i;
-        const uint32_t sb = sB + s * B_STAGE;
+        const uint32_t sb = s0 + i * d.st_bytes + d.st_boff;
         for (int row = tid >> 3; row < d.bn; row += 32) {
           const bf16 *src = Wt + (int64_t)(ct.n0 + row) * d.Kpad + kb * MT_BK + c * 8;
           cp_async16(sb + row * 128 + ((c ^ (row & 7)) << 4), src, true);
@@ -404,50 +404,59 @@ __device__ void conv_tc_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaSh
     sh.esh[tid] = n < d.Co ? __ldg(reinterpret_cast<const float *>(d.shift) + n) : 0.f;
   }
   // the rest of this split's weight rows -> L2 (one bulk prefetch per row)
-  if (ct.nk > MT_STAGES && tid < d.bn)
-    prefetch_l2_bulk(Wt + (int64_t)(ct.n0 + tid) * d.Kpad + (ct.kb0 + MT_STAGES) * MT_BK,
-                     (uint32_t)(ct.nk - MT_STAGES) * MT_BK * 2);
+  if (ct.nk > d.nst && tid < d.bn)
+    prefetch_l2_bulk(Wt + (int64_t)(ct.n0 + tid) * d.Kpad + (ct.kb0 + d.nst) * MT_BK,
+                     (uint32_t)(ct.nk - d.nst) * MT_BK * 2);
 }
 
 // TMA mainloop: thread 0 = producer (A boxes, and B beyond the prefetched stages), thread 32 =
-// MMA issuer (UMMA 128 x bn x 16 from the two SW128 stages, commit frees the stage), everyone
-// else waits for the accumulator.
+// MMA issuer (UMMA 128 x bn x 16 from the two SW128 tiles of a stage; commit frees the stage),
+// everyone else waits for the accumulator.
 __device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const ConvTile &ct, uint8_t *smem,
-                                                     CtaShared &sh, PipeState &ps) {
+                                                     CtaShared &sh, const PipeState &ps) {
   const int tid = threadIdx.x;
-  const uint32_t sA = smem_u32(smem), sB = sA + MT_STAGES * A_STAGE;
+  const uint32_t s0 = smem_u32(smem);
   const uint32_t bar_full0 = smem_u32(&sh.bar_full[0]);
   const uint32_t bar_empty0 = smem_u32(&sh.bar_empty[0]);
   const uint32_t bar_accf = smem_u32(&sh.bar_accf);
+  const int nst = d.nst;
+  // the role lanes (producer = lane 0 of warp 0, MMA issuer = lane 0 of warp 1) must not share
+  // their warp with lanes spinning on an mbarrier: the siblings park on __syncwarp instead
   if (tid == 0) {
     for (int i = 0; i < ct.nk; ++i) {
-      const uint32_t f = ps.fill + i;
-      const int s = f % MT_STAGES;
-      if (i >= MT_STAGES) {
-        mbar_wait(bar_empty0 + 8 * s, ((f / MT_STAGES) - 1) & 1);
+      const int s = i % nst, j = i / nst;
+      const uint32_t st = s0 + s * d.st_bytes;
+      if (j > 0) {
+        mbar_wait(bar_empty0 + 8 * s, stage_par(ps.eph, s, j - 1));
         mbar_expect_tx(bar_full0 + 8 * s, (uint32_t)(d.a_bytes + d.bn * 128));
-        tma_load_2d(sB + s * B_STAGE, d.tmap_b, bar_full0 + 8 * s, (ct.kb0 + i) * MT_BK, ct.n0);
+        tma_load_2d(st + d.st_boff, d.tmap_b, bar_full0 + 8 * s, (ct.kb0 + i) * MT_BK, ct.n0);
       }
-      tma_issue_a(d, ct, ct.kb0 + i, sA + s * A_STAGE, bar_full0 + 8 * s);
+      if (i == 1) sh.t_kb[0] = gtimer();
+      tma_issue_a(d, ct, ct.kb0 + i, st, bar_full0 + 8 * s);
+      if (i == 1) sh.t_kb[1] = gtimer();
+      if (i == 2) sh.t_kb[2] = gtimer();
+      if (i == 3) sh.t_is[0] = gtimer();
     }
+    sh.t_aissue = gtimer();
   } else if (tid == 32) {
     const uint32_t idesc = idesc_bf16(d.bn);
     const uint32_t tmem = sh.tmem_base;
-    uint32_t ph = ps.fullph;
     for (int i = 0; i < ct.nk; ++i) {
-      const uint32_t f = ps.fill + i;
-      const int s = f % MT_STAGES;
-      mbar_wait(bar_full0 + 8 * s, (ph >> s) & 1);
-      ph ^= 1u << s;
+      const int s = i % nst, j = i / nst;
+      mbar_wait(bar_full0 + 8 * s, stage_par(ps.fph, s, j));
+      if (i == 0) sh.t_first = gtimer();
+      if (i == 12) sh.t_kb[3] = gtimer();
       tc_fence_after();
-      const uint32_t ab = sA + s * A_STAGE, bb = sB + s * B_STAGE;
+      const uint32_t ab = s0 + s * d.st_bytes, bb = ab + d.st_boff;
 #pragma unroll
       for (int kk = 0; kk < MT_BK / 16; ++kk)
         tc_mma(tmem, sdesc_sw128(ab + kk * 32), sdesc_sw128(bb + kk * 32), idesc, (i > 0 || kk > 0) ? 1u : 0u);
       tc_commit(bar_empty0 + 8 * s);
     }
     tc_commit(bar_accf);
+    sh.t_lastmma = gtimer();
   }
+  if (tid < 64) __syncwarp();
 }
 
 // cp.async mainloop (small-channel convs, e.g. the 3->8-padded stems): all threads gather im2col
@@ -455,7 +464,7 @@ __device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const Conv
 // group NS + j holds A (and, for j >= NS, B) of k-block j, so wait_group<NS-1> at iteration
 // i = j + NS - 1 completes both the prefetched B of k-block j and its A.
 __device__ __forceinline__ void conv_tc_mainloop_cpasync(const RunArgs &a, const OpDesc &d, const ConvTile &ct,
-                                                         uint8_t *smem, CtaShared &sh, PipeState &ps) {
+                                                         uint8_t *smem, CtaShared &sh, const PipeState &ps) {
   const int tid = threadIdx.x;
   const int m0 = ct.m0, n0 = ct.n0, kb0 = ct.kb0, nk = ct.nk;
   const bf16 *X = in_ptr<bf16>(a, d);
@@ -475,23 +484,22 @@ __device__ __forceinline__ void conv_tc_mainloop_cpasync(const RunArgs &a, const
     hb[i] = ho * d.sh - d.ph;
     wb[i] = wo * d.sw - d.pw;
   }
-  const uint32_t sA = smem_u32(smem), sB = sA + MT_STAGES * A_STAGE;
+  const uint32_t s0 = smem_u32(smem);
   const uint32_t idesc = idesc_bf16(d.bn);
   const uint32_t tmem = sh.tmem_base;
   const uint32_t bar_empty0 = smem_u32(&sh.bar_empty[0]);
   const uint32_t bar_accf = smem_u32(&sh.bar_accf);
   for (int i = 0; i < nk + MT_STAGES - 1; ++i) {
     if (i < nk) {
-      const uint32_t f = ps.fill + i;
-      const int s = f % MT_STAGES;
-      if (i >= MT_STAGES) mbar_wait(bar_empty0 + 8 * s, ((f / MT_STAGES) - 1) & 1);
+      const int s = i % MT_STAGES, jj = i / MT_STAGES;
+      if (jj > 0) mbar_wait(bar_empty0 + 8 * s, stage_par(ps.eph, s, jj - 1));
       const int kb = kb0 + i;
       const int k = kb * MT_BK + c * 8;
       const bool kv = k < d.K;
       const int tap = kv ? k / d.C : 0;
       const int ci = k - tap * d.C;
       const int rr = tap / d.kw, ss = tap - rr * d.kw;
-      const uint32_t sa = sA + s * A_STAGE;
+      const uint32_t sa = s0 + s * d.st_bytes;
 #pragma unroll
       for (int i2 = 0; i2 < 4; ++i2) {
         const int row = (tid >> 3) + 32 * i2;
@@ -500,8 +508,8 @@ __device__ __forceinline__ void conv_tc_mainloop_cpasync(const RunArgs &a, const
         const bf16 *src = valid ? X + (int64_t)(pbase[i2] + hi * d.W + wi) * d.in_cs + d.in_co + ci : X;
         cp_async16(sa + row * 128 + ((c ^ (row & 7)) << 4), src, valid);
       }
-      if (i >= MT_STAGES) {
-        const uint32_t sb = sB + s * B_STAGE;
+      if (jj > 0) {
+        const uint32_t sb = sa + d.st_boff;
         for (int row = tid >> 3; row < d.bn; row += 32) {
           const bf16 *src = Wt + (int64_t)(n0 + row) * d.Kpad + kb * MT_BK + c * 8;
           cp_async16(sb + row * 128 + ((c ^ (row & 7)) << 4), src, true);
@@ -516,8 +524,8 @@ __device__ __forceinline__ void conv_tc_mainloop_cpasync(const RunArgs &a, const
       __syncthreads();
       if (tid == 0) {
         tc_fence_after();
-        const int s = (ps.fill + j) % MT_STAGES;
-        const uint32_t ab = sA + s * A_STAGE, bb = sB + s * B_STAGE;
+        const int s = j % MT_STAGES;
+        const uint32_t ab = s0 + s * d.st_bytes, bb = ab + d.st_boff;
 #pragma unroll
         for (int kk = 0; kk < MT_BK / 16; ++kk)
           tc_mma(tmem, sdesc_sw128(ab + kk * 32), sdesc_sw128(bb + kk * 32), idesc,
@@ -632,13 +640,17 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
   const ConvTile ct = conv_tile_coords(d, tile);
   const int tmn = ct.tmn, ks = ct.ks, n0 = ct.n0;
   const uint32_t bar_accf = smem_u32(&sh.bar_accf);
-  if (d.tma) {
-    conv_tc_mainloop_tma(d, ct, smem, sh, ps);
-    for (int i = 0; i < ct.nk; ++i) ps.fullph ^= 1u << ((ps.fill + i) % MT_STAGES);
-  } else {
-    conv_tc_mainloop_cpasync(a, d, ct, smem, sh, ps);
+  if (d.tma) conv_tc_mainloop_tma(d, ct, smem, sh, ps);
+  else conv_tc_mainloop_cpasync(a, d, ct, smem, sh, ps);
+  {   // stage s was used ceil((nk - s) / nst) times: flip its parities when odd
+    const int nst = d.tma ? d.nst : MT_STAGES;
+    for (int st = 0; st < nst && st < ct.nk; ++st) {
+      if ((((ct.nk - 1 - st) / nst) & 1) == 0) {
+        ps.eph ^= 1u << st;
+        if (d.tma) ps.fph ^= 1u << st;
+      }
+    }
   }
-  ps.fill += ct.nk;
   mbar_wait(bar_accf, ps.acc_phase);
   ps.acc_phase ^= 1;
   tc_fence_after();
@@ -1345,7 +1357,7 @@ __device__ __forceinline__ uint8_t *smem_base() {
 __device__ void cta_setup(CtaShared &sh, bool need_tmem) {
   const int tid = threadIdx.x;
   if (tid == 0) {
-    for (int s = 0; s < MT_STAGES; ++s) {
+    for (int s = 0; s < MT_MAXST; ++s) {
       mbar_init(smem_u32(&sh.bar_empty[s]), 1);
       mbar_init(smem_u32(&sh.bar_full[s]), 1);
     }
@@ -1413,7 +1425,7 @@ __device__ __forceinline__ void trace_tile(const RunArgs &a, const CtaShared &sh
   if ((int)i >= a.trace_cap) return;
   unsigned smid;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-  unsigned long long *e = a.trace + (size_t)i * 8;
+  unsigned long long *e = a.trace + (size_t)i * 16;
   e[0] = ((unsigned long long)(unsigned)tile << 32) | (unsigned)op;
   e[1] = ((unsigned long long)blockIdx.x << 32) | smid;
   e[2] = sh.t_pick;
@@ -1422,6 +1434,11 @@ __device__ __forceinline__ void trace_tile(const RunArgs &a, const CtaShared &sh
   e[5] = sh.t_run + (unsigned long long)sh.last;   // after the release
   e[6] = (unsigned long long)sh.home;
   e[7] = sh.t_run;
+  e[8] = sh.t_first;      // MMA thread: first stage landed
+  e[9] = sh.t_lastmma;    // MMA thread: last MMA issued
+  e[10] = sh.t_aissue;    // producer: last A box issued
+  e[11] = sh.t_kb[0]; e[12] = sh.t_kb[1]; e[13] = sh.t_kb[2]; e[14] = sh.t_kb[3];   // stages 1,4,8,12 landed
+  e[15] = sh.t_is[0];     // producer: 4th A box issued
 }
 
 // One stage.  Claim-then-wait: thread 0 claims the next unclaimed tile of the first op of its
@@ -1444,9 +1461,21 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
   while (true) {
     if (tid == 0) {
       int op = -1, tile = 0, ten = -1;
+      // visiting order: home tenant first; then (steal 1) round-robin or (steal 2) the tenant with
+      // the most unclaimed ops of its slice first (critical-path-first list scheduling)
+      int order[MT_MAXT];
+      order[0] = sh.home;
+      int no = 1;
+      for (int q = 1; q < T; ++q) order[no++] = (sh.home + q) % T;
+      if (a.steal == 2)
+        for (int i = 1; i < no; ++i)
+          for (int j = i + 1; j < no; ++j) {
+            const int ri = sh.end[order[i]] - sh.cur[order[i]], rj = sh.end[order[j]] - sh.cur[order[j]];
+            if (rj > ri) { const int x = order[i]; order[i] = order[j]; order[j] = x; }
+          }
       for (int q = 0; q < T && op < 0; ++q) {
         if (!a.steal && q > 0) break;
-        const int t = (sh.home + q) % T;
+        const int t = order[q];
         while (sh.cur[t] < sh.end[t]) {
           const int o = sh.cur[t];
           const int k = atomicAdd(a.claim + o, 1);
@@ -1458,7 +1487,8 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
       sh.tile = tile;
       sh.ten = ten;
       sh.t_pick = gtimer();
-      sh.t_mma = 0;
+      sh.t_mma = sh.t_first = sh.t_lastmma = sh.t_aissue = 0;
+      sh.t_kb[0] = sh.t_kb[1] = sh.t_kb[2] = sh.t_kb[3] = sh.t_is[0] = 0;
     }
     __syncthreads();
     const int op = sh.op;

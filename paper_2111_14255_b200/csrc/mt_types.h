@@ -7,7 +7,9 @@
 #define MT_MAXIN 8        // max inputs of one op (== MT_MAX_INPUTS)
 #define MT_MAXDEP 9       // inputs + residual
 #define MT_NTHREADS 256   // threads per CTA of every kernel
-#define MT_STAGES 4       // smem pipeline depth of the tcgen05 conv tile
+#define MT_STAGES 4       // smem pipeline depth of the cp.async conv mainloop (32 KB stages)
+#define MT_MAXST 12       // max pipeline depth of the TMA conv mainloop (stage = A box + B box)
+#define MT_PIPE_BYTES (192 * 1024)   // shared-memory ring of the conv pipeline
 #define MT_BM 128         // tcgen05 conv tile rows (output pixels), UMMA M
 #define MT_BK 64          // K per pipeline stage (one 128-byte swizzle atom of bf16)
 #define MT_SIMT_BM 64     // SIMT conv tile
@@ -57,7 +59,8 @@ struct OpDesc {
   int32_t a_bytes;                  // TMA: bytes of one A box (rows * Wo * 128)
   int32_t rc;                       // split-K: reduce tiles per (M,N) tile (32 columns each); the op's
                                     // tiles are [tmn*splits compute tiles][tmn*rc reduce tiles]
-  int32_t pad3;
+  int32_t nst;                      // conv pipeline: stages, bytes per stage, offset of B in a stage
+  int32_t st_bytes, st_boff, pad3;
   int32_t M, K, Kpad, nkb;          // GEMM view (conv / FC)
   int32_t bn, tiles_m, tiles_n, splits;
   int32_t kb_per_split, tiles, cnt_off, pad0;

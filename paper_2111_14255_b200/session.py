@@ -17,8 +17,8 @@ class TenantMix:
         self.graphs = graphs
         self.dev = torch.device("cuda", device)
         self.ctx = Context(device)
-        if not steal:
-            self.ctx.set_option(1, 0)
+        if steal is not True:
+            self.ctx.set_option(1, int(steal))
         self._params = []
         ptrs = []
         for g in graphs:

@@ -22,7 +22,10 @@ src_csv = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], captur
 rows = list(csv.reader(io.StringIO(src_csv)))
 hdr = rows[1]
 ia, isamp = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)")
-ins = [(int(r[ia], 16), int(r[isamp] or 0)) for r in rows[2:] if len(r) > isamp and r[ia].startswith("0x")]
+reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+ridx = [hdr.index(h) for h in reasons]
+ins = [(int(r[ia], 16), int(r[isamp] or 0), [int(r[k] or 0) for k in ridx]) for r in rows[2:]
+       if len(r) > isamp and r[ia].startswith("0x")]
 base = ins[0][0]
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.join(ROOT, "paper_2111_14255_b200", "libmt.so")], cwd=tmp,
@@ -48,12 +51,20 @@ for ln in dis.splitlines():
         line_of[int(m.group(1), 16)] = cur
 src = open(os.path.join(ROOT, "paper_2111_14255_b200", "csrc", "kernels.cu")).read().splitlines()
 agg = collections.Counter()
+why = collections.defaultdict(lambda: [0] * len(reasons))
 tot = 0
-for addr, smp in ins:
+for addr, smp, rs in ins:
     off = addr - base
-    agg[line_of.get(off, -1)] += smp
+    ln = line_of.get(off, -1)
+    agg[ln] += smp
+    for k, v in enumerate(rs):
+        why[ln][k] += v
     tot += smp
 print(f"{rep}: {tot} samples, {len(ins)} SASS instructions")
 for line, smp in agg.most_common(top):
     txt = src[line - 1].strip()[:90] if 0 < line <= len(src) else "?"
-    print(f"{smp:7d} {100.0 * smp / max(tot, 1):5.1f}%  L{line:<5d} {txt}")
+    w = why[line]
+    tw = sum(w) or 1
+    top3 = sorted(range(len(w)), key=lambda k: -w[k])[:2]
+    rs = " ".join(f"{reasons[k][6:]}:{100 * w[k] // tw}%" for k in top3)
+    print(f"{smp:7d} {100.0 * smp / max(tot, 1):5.1f}%  L{line:<5d} {txt[:70]:70s} [{rs}]")

@@ -22,7 +22,7 @@ ap.add_argument("--steal", type=int, default=1)
 a = ap.parse_args()
 g = configs.tenants(a.config)
 L = [x.n_ops for x in g]
-m = TenantMix(g, steal=bool(a.steal))
+m = TenantMix(g, steal=a.steal)
 m.set_input(zoo.make_input(g[0]))
 rho = {"all_concurrent": configs.all_concurrent_pointers, "sequential": configs.sequential_pointers,
        "uniform4": configs.uniform_pointers}[a.schedule](L)

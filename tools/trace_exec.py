@@ -24,7 +24,18 @@ ap.add_argument("--out", default=None)
 ap.add_argument("--top", type=int, default=30)
 ap.add_argument("--synthetic", default=None, help="dwchain | pwchain | gapchain")
 a = ap.parse_args()
-if a.synthetic:
+if a.synthetic and a.synthetic.startswith("pw:"):
+    # pw:CIN:COUT:HW  -> alternating 1x1 convs CIN->COUT->CIN at HWxHW
+    _, ci, co, hw = a.synthetic.split(":")
+    ci, co, hw = int(ci), int(co), int(hw)
+    b = zoo.GraphBuilder("tinyA", 1, ci, hw, hw, zoo.PREC_BF16, seed=0)
+    x = b.conv(-1, ci, 1, 1, 0)
+    for i in range(6):
+        x = b.conv(x, co, 1, 1, 0)
+        x = b.conv(x, ci, 1, 1, 0)
+    b.gap(x)
+    g = [b.build()]
+elif a.synthetic:
     b = zoo.GraphBuilder("tinyA", 1, 384, 14, 14, zoo.PREC_BF16, seed=0)
     x = b.conv(-1, 384, 1, 1, 0)
     for i in range(12):
@@ -47,7 +58,7 @@ m.ctx.set_schedule_pointers(rho)
 for _ in range(3):
     m.run()
 cap = 1 << 16
-buf = torch.zeros(cap * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(cap * 16, dtype=torch.int64, device="cuda")
 m.ctx.set_trace(buf.data_ptr(), cap)
 if a.baseline:
     total = m.ctx.run_baseline(a.baseline, m.in_ptrs, m.out_ptrs)
@@ -56,7 +67,7 @@ else:
     total, stages = m.run()
 n = m.ctx.trace_count()
 m.ctx.set_trace(0, 0)
-tr = buf[: n * 8].view(n, 8).cpu().numpy().astype(np.int64)
+tr = buf[: n * 16].view(n, 16).cpu().numpy().astype(np.int64)
 t0 = tr[:, 2].min()
 names = []
 for t, gg in enumerate(g):
@@ -90,3 +101,4 @@ busy = ((tr[:, 5] - tr[:, 3]).sum() / 1e3)
 print(f"SM-busy (work) us summed over CTAs: {busy:.1f}; makespan x CTAs: {total * 148:.1f} -> util {busy / (total * 148):.3f}")
 if a.out:
     json.dump(dict(total=total, stages=stages, rows=rows), open(a.out, "w"), indent=1)
+    np.save(a.out.replace(".json", "_raw.npy"), tr)

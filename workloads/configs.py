@@ -28,6 +28,10 @@ CONFIGS = {
     "zoo5": (("vgg16", "resnet18", "resnet34", "resnet50", "resnet101"), 1, zoo.PREC_BF16,
              "Table I VGG+R18+R34+R50+R101"),
     "alex_vgg_r18": (("alexnet", "vgg16", "resnet18"), 1, zoo.PREC_BF16, "Table II Alex+VGG+R18"),
+    # single tenants (profiling the per-op dependency chain)
+    "mbv2": (("mobilenet_v2",), 1, zoo.PREC_BF16, "MobileNet-V2 alone"),
+    "r18": (("resnet18",), 1, zoo.PREC_BF16, "ResNet-18 alone"),
+    "r50": (("resnet50",), 1, zoo.PREC_BF16, "ResNet-50 alone"),
 }
 
 
