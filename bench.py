@@ -281,24 +281,22 @@ def main():
         pmix.set_input(zoo.make_input(pg[0]))
         PL = [g.n_ops for g in pg]
         allc = configs.sample_candidates(PL, args.n_cand, seed=14255)
-        mine = [c for i, c in enumerate(allc) if i % ws == rank]
-        pmix.ctx.profile_batch_pointers(mine[:8], pmix.in_ptrs, pmix.out_ptrs, 1, 1, sp)  # warm
+        from paper_2111_14255_b200 import distributed as D
+        pfn = lambda cs: pmix.ctx.profile_batch_pointers(cs, pmix.in_ptrs, pmix.out_ptrs, 2, 10, sp)
+        pmix.ctx.profile_batch_pointers(allc[:8], pmix.in_ptrs, pmix.out_ptrs, 1, 1, sp)  # warm
         barrier()
         t0 = time.perf_counter()
-        lat_p, st_p = pmix.ctx.profile_batch_pointers(mine, pmix.in_ptrs, pmix.out_ptrs, 2, 10, sp)
-        if ws > 1:
-            n_loc = -(-args.n_cand // ws)
-            buf = torch.full((n_loc,), float("nan"), device=dev)
-            buf[:len(mine)] = torch.from_numpy(lat_p).to(dev)
-            gat = [torch.empty_like(buf) for _ in range(ws)]
-            dist.all_gather(gat, buf)
-            torch.cuda.synchronize(dev)
+        lat_all, st_all = D.profile_distributed(pfn, allc, rank, ws, device=dev)
+        torch.cuda.synchronize(dev)
         dt = maxall(time.perf_counter() - t0)
+        lat_p = lat_all[st_all == 0]
+        st_p = st_all
         prof_line = {"config": args.profile_config, "candidates": args.n_cand, "warmup": 2, "iters": 10,
                      "schedules_per_s": args.n_cand / dt, "wall_s": dt,
-                     "feasible_rank0": int((st_p == 0).sum()),
-                     "rank0_best_us": float(np.nanmin(lat_p)) if len(lat_p) else None,
-                     "rank0_median_us": float(np.nanmedian(lat_p)) if len(lat_p) else None}
+                     "feasible": int((st_p == 0).sum()),
+                     "best_us": float(np.nanmin(lat_p)) if len(lat_p) else None,
+                     "median_us": float(np.nanmedian(lat_p)) if len(lat_p) else None,
+                     "gather": "NCCL all_gather of per-rank latencies" if ws > 1 else "none (1 GPU)"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:

@@ -1,0 +1,66 @@
+"""Multi-process (world_size 2, gloo, CPU) test of the candidate-sharded profiling path: sharding,
+all_gather and un-permutation give every rank the same full result vector as a 1-rank run."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from workloads import configs
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _fake_profile(cands):
+    """stand-in for mt_profile_batch on CPU: a deterministic 'latency' per candidate and a status
+    (infeasible when some stage of the pointer matrix is empty for every tenant)"""
+    lat, st = [], []
+    for rho in cands:
+        key = sum((i + 1) * (k + 3) * v for i, row in enumerate(rho) for k, v in enumerate(row))
+        lat.append(100.0 + (key % 997) * 0.5)
+        st.append(0 if key % 13 else 2)
+    return np.array(lat, np.float32), np.array(st, np.int32)
+
+
+def _worker(rank, world, port, n, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2111_14255_b200 import distributed as D
+    cands = configs.sample_candidates([56, 21, 54], n, seed=14255)
+    lat, st = D.profile_distributed(_fake_profile, cands, rank, world)
+    out[rank] = (lat.tolist(), st.tolist())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [17, 64])
+def test_sharded_profile_gather_gloo_world2(n):
+    pytest.importorskip("paper_2111_14255_b200.mt")
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_worker, args=(2, port, n, out), nprocs=2, join=True)
+        res = dict(out)
+    ref_lat, ref_st = _fake_profile(configs.sample_candidates([56, 21, 54], n, seed=14255))
+    for r in (0, 1):
+        lat, st = res[r]
+        np.testing.assert_array_equal(np.array(lat, np.float32), ref_lat)
+        np.testing.assert_array_equal(np.array(st, np.int32), ref_st)
+
+
+def test_shard_indices_partition():
+    from paper_2111_14255_b200 import distributed as D
+    for n in (0, 1, 7, 1024):
+        for w in (1, 2, 3, 8):
+            allc = sorted(c for r in range(w) for c in D.shard_indices(n, r, w))
+            assert allc == list(range(n))
