@@ -423,35 +423,47 @@ __device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const Conv
   // the role lanes (producer = lane 0 of warp 0, MMA issuer = lane 0 of warp 1) must not share
   // their warp with lanes spinning on an mbarrier: the siblings park on __syncwarp instead
   if (tid == 0) {
+    // incremental stage / tap / channel-block counters (no divisions in the issue loop)
+    const uint32_t txb = (uint32_t)(d.a_bytes + d.bn * 128);
+    const int kb0 = ct.kb0;
+    int tap = kb0 / d.cblks, cb = kb0 - tap * d.cblks;
+    int rr = tap / d.kw, ss = tap - rr * d.kw;
+    const int hbase = ct.ho0 * d.sh - d.ph;
+    int s = 0, j = 0;
+    uint32_t st = s0;
     for (int i = 0; i < ct.nk; ++i) {
-      const int s = i % nst, j = i / nst;
-      const uint32_t st = s0 + s * d.st_bytes;
       if (j > 0) {
         mbar_wait(bar_empty0 + 8 * s, stage_par(ps.eph, s, j - 1));
-        mbar_expect_tx(bar_full0 + 8 * s, (uint32_t)(d.a_bytes + d.bn * 128));
-        tma_load_2d(st + d.st_boff, d.tmap_b, bar_full0 + 8 * s, (ct.kb0 + i) * MT_BK, ct.n0);
+        mbar_expect_tx(bar_full0 + 8 * s, txb);
+        tma_load_2d(st + d.st_boff, d.tmap_b, bar_full0 + 8 * s, (kb0 + i) * MT_BK, ct.n0);
       }
-      if (i == 1) sh.t_kb[0] = gtimer();
-      tma_issue_a(d, ct, ct.kb0 + i, st, bar_full0 + 8 * s);
-      if (i == 1) sh.t_kb[1] = gtimer();
-      if (i == 2) sh.t_kb[2] = gtimer();
+      tma_load_4d(st, d.tmap_a, bar_full0 + 8 * s, cb * 64, ss - d.pw, hbase + rr, ct.img);
       if (i == 3) sh.t_is[0] = gtimer();
+      if (++cb == d.cblks) {
+        cb = 0;
+        if (++ss == d.kw) { ss = 0; ++rr; }
+      }
+      st += d.st_bytes;
+      if (++s == nst) { s = 0; ++j; st = s0; }
     }
     sh.t_aissue = gtimer();
   } else if (tid == 32) {
     const uint32_t idesc = idesc_bf16(d.bn);
     const uint32_t tmem = sh.tmem_base;
+    int s = 0, j = 0;
+    uint32_t ab = s0;
     for (int i = 0; i < ct.nk; ++i) {
-      const int s = i % nst, j = i / nst;
       mbar_wait(bar_full0 + 8 * s, stage_par(ps.fph, s, j));
       if (i == 0) sh.t_first = gtimer();
       if (i == 12) sh.t_kb[3] = gtimer();
       tc_fence_after();
-      const uint32_t ab = s0 + s * d.st_bytes, bb = ab + d.st_boff;
+      const uint32_t bb = ab + d.st_boff;
 #pragma unroll
       for (int kk = 0; kk < MT_BK / 16; ++kk)
         tc_mma(tmem, sdesc_sw128(ab + kk * 32), sdesc_sw128(bb + kk * 32), idesc, (i > 0 || kk > 0) ? 1u : 0u);
       tc_commit(bar_empty0 + 8 * s);
+      ab += d.st_bytes;
+      if (++s == nst) { s = 0; ++j; ab = s0; }
     }
     tc_commit(bar_accf);
     sh.t_lastmma = gtimer();
@@ -1496,60 +1508,78 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
     load_desc(sh, a.ops + op);
     __syncthreads();
     tile_prefetch(sh.d, sh.tile, smem, sh, ps);
-    if (tid == 0) {
+    if (tid < 32) {
       // wait for exactly the producer pixel blocks this tile reads (tile-level dataflow between
-      // consecutive ops of a tenant); whole producer ops already seen complete are cached
-      int ok = 1;
+      // consecutive ops of a tenant).  Warp 0 polls in parallel: lane k checks whether dependency
+      // k is complete as a whole (cached per CTA), then, per incomplete dependency, the lanes poll
+      // its blocks together -- one L2 round trip when everything is already there.
+      const int lane = tid;
       const OpDesc &d = sh.d;
-      int64_t p0, p1, i0, i1;
-      tile_out_range(d, sh.tile, p0, p1);
-      tile_in_range(d, p0, p1, i0, i1);
-      const unsigned long long t0 = gtimer();
-      unsigned spins = 0;
-      for (int k = 0; k < d.n_dep && ok; ++k) {
-        const int dep = d.deps[k];
-        if (dep < 2048 && (sh.complete[dep >> 5] >> (dep & 31) & 1u)) continue;
-        const OpDesc *pd = a.ops + dep;
-        if (ld_acquire(a.done + dep) >= __ldg(&pd->tiles)) {
-          if (dep < 2048) sh.complete[dep >> 5] |= 1u << (dep & 31);
-          continue;
+      int ok = 1;
+      bool incomplete = false;
+      if (lane < d.n_dep) {
+        const int dep = d.deps[lane];
+        const bool cached = dep < 2048 && ((sh.complete[dep >> 5] >> (dep & 31)) & 1u);
+        if (!cached) {
+          if (ld_acquire(a.done + dep) >= __ldg(&a.ops[dep].tiles)) {
+            if (dep < 2048) atomicOr(&sh.complete[dep >> 5], 1u << (dep & 31));
+          } else {
+            incomplete = true;
+          }
         }
-        int64_t lo = INT64_MAX, hi = 0;
+      }
+      unsigned todo = __ballot_sync(0xffffffffu, incomplete);
+      if (todo) {
+        int64_t p0, p1, i0, i1;
+        tile_out_range(d, sh.tile, p0, p1);
+        tile_in_range(d, p0, p1, i0, i1);
         bool need_in = true, need_res = true;
         if (d.tk == TK_CONV_TC && d.splits > 1) {
           const bool red_tile = sh.tile >= d.tiles_m * d.tiles_n * d.splits;
           need_in = !red_tile;   // compute parts read the input only,
           need_res = red_tile;   // reduce tiles (epilogue) the residual only
         }
-        if ((d.dep_kind[k] & 1) && need_in) { lo = i0; hi = i1; }
-        if ((d.dep_kind[k] & 2) && need_res) { lo = min(lo, p0); hi = max(hi, p1); }
-        if (hi <= lo) continue;
-        const int need = __ldg(&pd->blk_need), off = __ldg(&pd->blk_off), nbk = __ldg(&pd->nblk);
-        int b0, b1;
-        const int br = __ldg(&pd->blk_rows);
-        if (br > 0) {   // producer blocks are whole-row M tiles: block = n * tpi + ho / rows
-          const int pWo = __ldg(&pd->Wo), pHoWo = __ldg(&pd->Ho) * pWo, tpi = __ldg(&pd->blk_tpi);
-          const int na = (int)(lo / pHoWo), nb2 = (int)((hi - 1) / pHoWo);
-          b0 = na * tpi + (int)((lo - (int64_t)na * pHoWo) / pWo) / br;
-          b1 = nb2 * tpi + (int)((hi - 1 - (int64_t)nb2 * pHoWo) / pWo) / br;
-        } else {
-          const int pb = __ldg(&pd->pix_blk);
-          b0 = (int)(lo / pb);
-          b1 = (int)((hi - 1) / pb);
-        }
-        b1 = min(nbk - 1, b1);
-        for (int b = b0; b <= b1 && ok; ++b) {
-          while (ld_acquire(a.blkcnt + off + b) < need) {
-            if ((++spins & 255) == 0) {
-              if (ld_acquire_u(&a.ctl->error)) { ok = 0; break; }
-              if (gtimer() - t0 > a.timeout_ns) { atomicExch(&a.ctl->error, 2u); ok = 0; break; }
+        const unsigned long long t0 = gtimer();
+        unsigned spins = 0;
+        while (todo) {
+          const int k = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const int dep = d.deps[k];
+          const OpDesc *pd = a.ops + dep;
+          int64_t lo = INT64_MAX, hi = 0;
+          if ((d.dep_kind[k] & 1) && need_in) { lo = i0; hi = i1; }
+          if ((d.dep_kind[k] & 2) && need_res) { lo = min(lo, p0); hi = max(hi, p1); }
+          if (hi <= lo) continue;
+          const int need = __ldg(&pd->blk_need), off = __ldg(&pd->blk_off), nbk = __ldg(&pd->nblk);
+          int b0, b1;
+          const int br = __ldg(&pd->blk_rows);
+          if (br > 0) {   // producer blocks are whole-row M tiles: block = n * tpi + ho / rows
+            const int pWo = __ldg(&pd->Wo), pHoWo = __ldg(&pd->Ho) * pWo, tpi = __ldg(&pd->blk_tpi);
+            const int na = (int)(lo / pHoWo), nb2 = (int)((hi - 1) / pHoWo);
+            b0 = na * tpi + (int)((lo - (int64_t)na * pHoWo) / pWo) / br;
+            b1 = nb2 * tpi + (int)((hi - 1 - (int64_t)nb2 * pHoWo) / pWo) / br;
+          } else {
+            const int pb = __ldg(&pd->pix_blk);
+            b0 = (int)(lo / pb);
+            b1 = (int)((hi - 1) / pb);
+          }
+          b1 = min(nbk - 1, b1);
+          for (int b = b0 + lane; b <= b1 && ok; b += 32) {
+            while (ld_acquire(a.blkcnt + off + b) < need) {
+              if ((++spins & 255) == 0) {
+                if (ld_acquire_u(&a.ctl->error)) { ok = 0; break; }
+                if (gtimer() - t0 > a.timeout_ns) { atomicExch(&a.ctl->error, 2u); ok = 0; break; }
+              }
+              __nanosleep(20);
             }
-            __nanosleep(20);
           }
         }
       }
-      sh.ok = ok;
-      sh.t_deps = gtimer();
+      ok = __all_sync(0xffffffffu, ok);
+      if (lane == 0) {
+        sh.ok = ok;
+        sh.t_deps = gtimer();
+      }
     }
     __syncthreads();
     if (!sh.ok) { cp_async_wait<0>(); return false; }
