@@ -34,7 +34,8 @@ struct CtaShared {
   unsigned long long bar_accf;
   uint32_t tmem_base;
   int op, tile, last, ok, home, ten;
-  unsigned long long t_pick, t_deps, t_mma, t_run, t_first, t_lastmma, t_aissue;
+  int smem_cap;               // bytes of dynamic shared memory this kernel has (staging budget)
+  unsigned long long t_pick, t_pick_next, t_deps, t_mma, t_run, t_first, t_lastmma, t_aissue;
   unsigned long long t_kb[4], t_is[1];
   int cur[MT_MAXT], end[MT_MAXT];
   uint32_t complete[64];      // bitset of ops observed fully complete (global op id < 2048)
@@ -232,6 +233,17 @@ __device__ __forceinline__ Raw8<float> ldraw_nc(const float *p) {
   Raw8<float> r;
   r.a = __ldg(reinterpret_cast<const float4 *>(p));
   r.b = __ldg(reinterpret_cast<const float4 *>(p + 4));
+  return r;
+}
+__device__ __forceinline__ Raw8<bf16> ldraw_gen(const bf16 *p) {   // generic: smem or global
+  Raw8<bf16> r;
+  r.u = *reinterpret_cast<const uint4 *>(p);
+  return r;
+}
+__device__ __forceinline__ Raw8<float> ldraw_gen(const float *p) {
+  Raw8<float> r;
+  r.a = reinterpret_cast<const float4 *>(p)[0];
+  r.b = reinterpret_cast<const float4 *>(p)[1];
   return r;
 }
 __device__ __forceinline__ void zero_raw(Raw8<bf16> &r) { r.u = make_uint4(0, 0, 0, 0); }
@@ -874,6 +886,14 @@ __device__ __forceinline__ void dw_item(const RunArgs &a, const OpDesc &d, const
   store_out8<T>(a, d, pix, g * 8, acc, 8);
 }
 
+__device__ __forceinline__ bool dw3_staged(const OpDesc &d, int cap) {
+  return d.kh == 3 && d.kw == 3 && d.sh == d.sw && (d.sh == 1 || d.sh == 2) && d.pix_tile % d.Wo == 0 &&
+         11 * d.C * 4 <= cap;
+}
+__device__ __forceinline__ bool fc_staged(const OpDesc &d, int cap) {
+  const int64_t b = (int64_t)MT_FC_ROWS * d.K * (d.prec == 1 ? 4 : 2);
+  return b <= 96 * 1024 && b <= cap;
+}
 // packed fp32x2 FMA (sm_100 FFMA2): per lane identical to fmaf, so results are unchanged
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   unsigned long long r;
@@ -910,12 +930,14 @@ __device__ __forceinline__ Raw8<float> ldraw_cg_pred(const float *p, bool ok) {
 // A tile = whole output rows (pix_tile = rows * Wo); item = (row, run segment, channel group),
 // channel group fastest for coalescing.
 template <typename T, int S, int RUN>
-__device__ void dw3_tile(const RunArgs &a, const OpDesc &d, int tile) {
+__device__ void dw3_tile(const RunArgs &a, const OpDesc &d, int tile, const uint8_t *smem) {
   constexpr int NC = (RUN - 1) * S + 3;
   const T *X = in_ptr<T>(a, d);
-  const float *Wt = reinterpret_cast<const float *>(d.w);
-  const float *sc = reinterpret_cast<const float *>(d.scale);
-  const float *sf = reinterpret_cast<const float *>(d.shift);
+  cp_async_wait<0>();   // weights / scale / shift staged by tile_prefetch during the dependency wait
+  __syncthreads();
+  const float *Wt = reinterpret_cast<const float *>(smem);
+  const float *sc = Wt + 9 * d.C;
+  const float *sf = Wt + 10 * d.C;
   const int cg = d.C >> 3;
   const int nseg = (d.Wo + RUN - 1) / RUN;
   const int rows = d.pix_tile / d.Wo;
@@ -953,8 +975,8 @@ __device__ void dw3_tile(const RunArgs &a, const OpDesc &d, int tile) {
       float2 w2[3][4];   // this kernel row's 3 taps (fp32 weights, [9][C])
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
-        const float4 lo = __ldg(reinterpret_cast<const float4 *>(Wt + (r * 3 + t) * d.C + g * 8));
-        const float4 hi = __ldg(reinterpret_cast<const float4 *>(Wt + (r * 3 + t) * d.C + g * 8) + 1);
+        const float4 lo = reinterpret_cast<const float4 *>(Wt + (r * 3 + t) * d.C + g * 8)[0];
+        const float4 hi = reinterpret_cast<const float4 *>(Wt + (r * 3 + t) * d.C + g * 8)[1];
         w2[t][0] = make_float2(lo.x, lo.y); w2[t][1] = make_float2(lo.z, lo.w);
         w2[t][2] = make_float2(hi.x, hi.y); w2[t][3] = make_float2(hi.z, hi.w);
       }
@@ -975,10 +997,10 @@ __device__ void dw3_tile(const RunArgs &a, const OpDesc &d, int tile) {
     }
     float2 sc2[4], sf2[4];
     {
-      const float4 a0 = __ldg(reinterpret_cast<const float4 *>(sc + g * 8));
-      const float4 a1 = __ldg(reinterpret_cast<const float4 *>(sc + g * 8) + 1);
-      const float4 b0 = __ldg(reinterpret_cast<const float4 *>(sf + g * 8));
-      const float4 b1 = __ldg(reinterpret_cast<const float4 *>(sf + g * 8) + 1);
+      const float4 a0 = reinterpret_cast<const float4 *>(sc + g * 8)[0];
+      const float4 a1 = reinterpret_cast<const float4 *>(sc + g * 8)[1];
+      const float4 b0 = reinterpret_cast<const float4 *>(sf + g * 8)[0];
+      const float4 b1 = reinterpret_cast<const float4 *>(sf + g * 8)[1];
       sc2[0] = make_float2(a0.x, a0.y); sc2[1] = make_float2(a0.z, a0.w);
       sc2[2] = make_float2(a1.x, a1.y); sc2[3] = make_float2(a1.z, a1.w);
       sf2[0] = make_float2(b0.x, b0.y); sf2[1] = make_float2(b0.z, b0.w);
@@ -1001,10 +1023,10 @@ __device__ void dw3_tile(const RunArgs &a, const OpDesc &d, int tile) {
 }
 
 template <typename T>
-__device__ void dw_tile(const RunArgs &a, const OpDesc &d, int tile) {
-  if (d.kh == 3 && d.kw == 3 && d.sh == d.sw && (d.sh == 1 || d.sh == 2) && d.pix_tile % d.Wo == 0) {
-    if (d.sh == 1) dw3_tile<T, 1, 4>(a, d, tile);
-    else dw3_tile<T, 2, 2>(a, d, tile);
+__device__ void dw_tile(const RunArgs &a, const OpDesc &d, int tile, const uint8_t *smem, int cap) {
+  if (dw3_staged(d, cap)) {
+    if (d.sh == 1) dw3_tile<T, 1, 4>(a, d, tile, smem);
+    else dw3_tile<T, 2, 2>(a, d, tile, smem);
     return;
   }
   const T *X = in_ptr<T>(a, d);
@@ -1146,7 +1168,7 @@ __device__ __forceinline__ void fc_rows(const OpDesc &d, const T *X, const T *Wr
   for (; k8 + 32 * (U - 1) < K8; k8 += 32 * U) {
     Raw8<T> wr[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) wr[u] = ldraw_nc(Wr + (int64_t)(k8 + 32 * u) * 8);
+    for (int u = 0; u < U; ++u) wr[u] = ldraw_gen(Wr + (int64_t)(k8 + 32 * u) * 8);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       float w[8];
@@ -1164,7 +1186,7 @@ __device__ __forceinline__ void fc_rows(const OpDesc &d, const T *X, const T *Wr
   }
   for (; k8 < K8; k8 += 32) {
     float w[8];
-    ld8_nc(Wr + (int64_t)k8 * 8, w);
+    cvt8(ldraw_gen(Wr + (int64_t)k8 * 8), w);
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       if (NB == 1 || b < nb) {
@@ -1178,7 +1200,12 @@ __device__ __forceinline__ void fc_rows(const OpDesc &d, const T *X, const T *Wr
 }
 
 template <typename T>
-__device__ void fc_tile(const RunArgs &a, const OpDesc &d, int tile) {
+__device__ void fc_tile(const RunArgs &a, const OpDesc &d, int tile, const uint8_t *smem, int cap) {
+  const bool staged = fc_staged(d, cap);
+  if (staged) {   // weight rows staged by tile_prefetch during the dependency wait
+    cp_async_wait<0>();
+    __syncthreads();
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rb = (int)(tile % ((d.Co + MT_FC_ROWS - 1) / MT_FC_ROWS));
   const int bb = (int)(tile / ((d.Co + MT_FC_ROWS - 1) / MT_FC_ROWS));
@@ -1187,7 +1214,8 @@ __device__ void fc_tile(const RunArgs &a, const OpDesc &d, int tile) {
   const int b0 = bb * MT_FC_BATCH;
   const int nb = min(MT_FC_BATCH, d.N - b0);
   const T *X = in_ptr<T>(a, d);
-  const T *Wr = reinterpret_cast<const T *>(d.w) + (int64_t)o * d.K;
+  const T *Wr = staged ? reinterpret_cast<const T *>(smem) + (int64_t)warp * d.K
+                       : reinterpret_cast<const T *>(d.w) + (int64_t)o * d.K;
   float acc[MT_FC_BATCH];
 #pragma unroll
   for (int b = 0; b < MT_FC_BATCH; ++b) acc[b] = 0.f;
@@ -1274,10 +1302,10 @@ __device__ void run_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_t *s
       if (f32) conv_simt_tile<float>(a, d, tile, smem);
       else conv_simt_tile<bf16>(a, d, tile, smem);
       break;
-    case TK_DW: if (f32) dw_tile<float>(a, d, tile); else dw_tile<bf16>(a, d, tile); break;
+    case TK_DW: if (f32) dw_tile<float>(a, d, tile, smem, sh.smem_cap); else dw_tile<bf16>(a, d, tile, smem, sh.smem_cap); break;
     case TK_POOL: if (f32) pool_tile<float>(a, d, tile); else pool_tile<bf16>(a, d, tile); break;
     case TK_GAP: if (f32) gap_tile<float>(a, d, tile, smem); else gap_tile<bf16>(a, d, tile, smem); break;
-    case TK_FC: if (f32) fc_tile<float>(a, d, tile); else fc_tile<bf16>(a, d, tile); break;
+    case TK_FC: if (f32) fc_tile<float>(a, d, tile, smem, sh.smem_cap); else fc_tile<bf16>(a, d, tile, smem, sh.smem_cap); break;
     case TK_ELT: if (f32) elt_tile<float>(a, d, tile); else elt_tile<bf16>(a, d, tile); break;
     default: break;
   }
@@ -1338,7 +1366,30 @@ __device__ __forceinline__ int tile_block(const OpDesc &d, int tile, const CtaSh
 }
 
 // work that needs no producer data: issued before the dependency wait so it overlaps it
+// copy n16 16-byte chunks global -> shared with cp.async (completion waited in the tile)
+__device__ __forceinline__ void stage_smem(uint32_t dst, const void *src, int n16) {
+  for (int i = threadIdx.x; i < n16; i += MT_NTHREADS)
+    cp_async16(dst + i * 16, reinterpret_cast<const char *>(src) + (int64_t)i * 16, true);
+}
+
 __device__ void tile_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaShared &sh, const PipeState &ps) {
+  if (d.tk == TK_DW && dw3_staged(d, sh.smem_cap)) {   // [9][C] fp32 weights, scale[C], shift[C]
+    const uint32_t s0 = smem_u32(smem);
+    stage_smem(s0, reinterpret_cast<const void *>(d.w), 9 * d.C * 4 / 16);
+    stage_smem(s0 + 9 * d.C * 4, reinterpret_cast<const void *>(d.scale), d.C * 4 / 16);
+    stage_smem(s0 + 10 * d.C * 4, reinterpret_cast<const void *>(d.shift), d.C * 4 / 16);
+    cp_async_commit();
+    return;
+  }
+  if (d.tk == TK_FC && fc_staged(d, sh.smem_cap)) {     // the tile's weight rows
+    const int rb = (int)(tile % ((d.Co + MT_FC_ROWS - 1) / MT_FC_ROWS));
+    const int rows = min(MT_FC_ROWS, d.Co - rb * MT_FC_ROWS);
+    const int eb = d.prec == 1 ? 4 : 2;
+    stage_smem(smem_u32(smem), reinterpret_cast<const char *>(d.w) + (int64_t)rb * MT_FC_ROWS * d.K * eb,
+               (int)((int64_t)rows * d.K * eb / 16));
+    cp_async_commit();
+    return;
+  }
   if (d.tk == TK_CONV_TC) {
     if (d.splits > 1 && tile >= d.tiles_m * d.tiles_n * d.splits) return;   // reduce tile
     conv_tc_prefetch(d, tile, smem, sh, ps);
@@ -1471,7 +1522,8 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
   }
   __syncthreads();
   while (true) {
-    if (tid == 0) {
+    // thread 32 picks the next tile while thread 0 is still releasing the previous one
+    if (tid == 32) {
       int op = -1, tile = 0, ten = -1;
       // visiting order: home tenant first; then (steal 1) round-robin or (steal 2) the tenant with
       // the most unclaimed ops of its slice first (critical-path-first list scheduling)
@@ -1498,13 +1550,17 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
       sh.op = op;
       sh.tile = tile;
       sh.ten = ten;
-      sh.t_pick = gtimer();
-      sh.t_mma = sh.t_first = sh.t_lastmma = sh.t_aissue = 0;
-      sh.t_kb[0] = sh.t_kb[1] = sh.t_kb[2] = sh.t_kb[3] = sh.t_is[0] = 0;
+      sh.t_pick_next = gtimer();
     }
     __syncthreads();
     const int op = sh.op;
+    const int my_tile = sh.tile;
     if (op < 0) return true;
+    if (tid == 0) {
+      sh.t_pick = sh.t_pick_next;
+      sh.t_mma = sh.t_first = sh.t_lastmma = sh.t_aissue = 0;
+      sh.t_kb[0] = sh.t_kb[1] = sh.t_kb[2] = sh.t_kb[3] = sh.t_is[0] = 0;
+    }
     load_desc(sh, a.ops + op);
     __syncthreads();
     tile_prefetch(sh.d, sh.tile, smem, sh, ps);
@@ -1583,14 +1639,17 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
     }
     __syncthreads();
     if (!sh.ok) { cp_async_wait<0>(); return false; }
-    run_tile(a, sh.d, sh.tile, smem, sh, ps);
+    run_tile(a, sh.d, my_tile, smem, sh, ps);
     if (tid == 0) {   // publish: this tile's outputs are visible (release)
       sh.t_run = gtimer();
-      const int b = tile_block(sh.d, sh.tile, sh);
-      if (b >= 0) red_release_add(a.blkcnt + sh.d.blk_off + b, 1);
+      const int b = tile_block(sh.d, my_tile, sh);
+      const int boff = sh.d.blk_off;
+      if (b >= 0) red_release_add(a.blkcnt + boff + b, 1);
       red_release_add(a.done + op, 1);
-      if (a.trace) sh.last = (int)(gtimer() - sh.t_run);
-      trace_tile(a, sh, op, sh.tile);
+      if (a.trace) {
+        sh.last = (int)(gtimer() - sh.t_run);
+        trace_tile(a, sh, op, my_tile);
+      }
     }
   }
 }
@@ -1600,6 +1659,7 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
   __shared__ __align__(16) CtaShared sh;
   PipeState ps{0u, 0u, 0u};
   if (threadIdx.x < 64) sh.complete[threadIdx.x] = 0u;
+  if (threadIdx.x == 0) sh.smem_cap = PIPE_BYTES;
   cta_setup(sh, true);
   bool ok = grid_barrier(a, sh);
   if (ok) {
@@ -1639,6 +1699,7 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) op_kernel(RunArgs a, int op) {
   __shared__ __align__(16) CtaShared sh;
   PipeState ps{0u, 0u, 0u};
   load_desc(sh, a.ops + op);
+  if (threadIdx.x == 0) sh.smem_cap = PIPE_BYTES;
   const bool tc = __ldg(&a.ops[op].tk) == TK_CONV_TC;
   cta_setup(sh, tc);
   for (int t = blockIdx.x; t < sh.d.tiles; t += gridDim.x) {
@@ -1653,13 +1714,14 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) op_kernel(RunArgs a, int op) {
 }
 
 // small-smem variant for non-tensor-core ops so several op kernels can share an SM
-static constexpr int SMALL_SMEM = 1024 + MT_SIMT_BK * (MT_SIMT_BM + MT_SIMT_BN) * 4;
+static constexpr int SMALL_SMEM = 47 * 1024;   // <= 48 KB: no opt-in needed; 46 KB usable after alignment
 __global__ void __launch_bounds__(MT_NTHREADS) op_kernel_small(RunArgs a, int op) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(16) CtaShared sh;
   PipeState ps{0u, 0u, 0u};
   load_desc(sh, a.ops + op);
+  if (threadIdx.x == 0) sh.smem_cap = SMALL_SMEM - 1024;
   __syncthreads();
   for (int t = blockIdx.x; t < sh.d.tiles; t += gridDim.x) {
     if (threadIdx.x == 0) { sh.t_pick = gtimer(); sh.t_mma = 0; sh.home = -1; }
@@ -1742,6 +1804,8 @@ static cudaError_t set_attrs() {
   cudaError_t e = cudaFuncSetAttribute(executor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(op_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(op_kernel_small, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM);
   if (e != cudaSuccess) return e;
   done = true;
   return cudaSuccess;
