@@ -397,29 +397,50 @@ static mt_status plan_graphs(mt_ctx *c) {
               d.Kpad = d.nkb * MT_BK;
               d.K = d.Kpad;
               d.a_bytes = Rrows * os.w * 128;
+            } else if (d.C == 8 && os.w <= 128 && os.w * n.sw <= 256 && Rrows >= 1 && Rrows * n.sh <= 256 &&
+                       (!iv.graph_in || g.in_c <= 8)) {
+              // 8-channel input (the padded 3-channel stems): one 16-byte-row box per filter tap,
+              // 8 taps per K-block, canonical no-swizzle K-major layout
+              d.tma = 2;
+              d.blk_rows = Rrows;
+              d.blk_tpi = (int)cdiv(os.h, Rrows);
+              d.tiles_m = g.batch * d.blk_tpi;
+              d.cblks = 1;
+              d.K = n.kh * n.kw * 8;
+              d.Kpad = (int)rup(d.K, MT_BK);
+              d.nkb = d.Kpad / MT_BK;
+              d.a_bytes = 8 * Rrows * os.w * 16;
+              if (iv.graph_in) tn.tma_input = true;
             } else {
               d.K = n.kh * n.kw * d.C;
               d.Kpad = (int)rup(d.K, MT_BK);
               d.nkb = d.Kpad / MT_BK;
               d.tiles_m = (int)cdiv(d.M, MT_BM);
             }
-            // (bn, splits) from a latency model of one op at b=1..8 (shape-only, so outputs are
-            // schedule-invariant): waves x tile time (+ a reduce hop when split), with ~74 SMs
-            // available to the op (two tenants sharing the GPU).  Per-k-block and epilogue costs are
-            // the measured executor-trace figures.
+            // (bn, splits) from a latency model of one op (shape-only, so outputs are schedule-
+            // invariant), calibrated on executor traces: a tile streams its
+            // A box + B box per k-block at ~160 B/ns per SM (TMA) or pays the MMA time, whichever is
+            // larger; ~2.6 us of fixed cost per tile (dependency -> first data, epilogue); a split
+            // adds a dependent reduce hop (~4 us fixed + the partials at ~50 B/ns per reduce tile);
+            // ~74 SMs available to the op (two tenants sharing the GPU).
             int best_bn = d.bn, splits = 1;
             {
               double best = 1e30;
               const int bn_max = d.bn;
+              const double a_kb = d.tma ? (double)d.a_bytes : 16384.0;   // bytes of A per k-block
+              const double rows = d.tma ? (double)d.blk_rows * os.w : 128.0;
               for (int bn = bn_max; bn >= 32 || bn == bn_max; bn >>= 1) {
                 const int64_t tn = cdiv(os.c, bn), tmn_c = (int64_t)d.tiles_m * tn;
-                const double t_kb = 0.09 + 0.0006 * bn, t_epi = 0.5 + 0.02 * bn;
+                const double t_kb = std::max(0.13 * bn / 128.0, (a_kb + bn * 128.0) / 160000.0);
                 for (int sp = 1; sp <= 12; ++sp) {
-                  if (sp > 1 && d.nkb / sp < 4) break;
+                  if (sp > 1 && d.nkb / sp < 2) break;
                   const int64_t kbps = cdiv(d.nkb, sp);
                   const int64_t waves = cdiv(tmn_c * sp, 74);
-                  double t = waves * (0.8 + kbps * t_kb + (sp == 1 ? t_epi : 0.4));
-                  if (sp > 1) t += 2.0 + cdiv(tmn_c * std::max(1, bn / 32), 74) * (0.8 + 0.04 * sp * bn / 32.0);
+                  double t = waves * (1.3 + kbps * t_kb + (sp == 1 ? 1.3 + 0.01 * bn : 0.6));
+                  if (sp > 1) {
+                    const int rcn = std::max(1, bn / 32);
+                    t += 4.0 + cdiv(tmn_c * rcn, 74) * (sp * rows * 32 * 4 / 50000.0);
+                  }
                   if (t < best * 0.97) { best = t; best_bn = bn; splits = sp; }
                 }
                 if (bn <= 32) break;
@@ -432,7 +453,7 @@ static mt_status plan_graphs(mt_ctx *c) {
             d.splits = (int)cdiv(d.nkb, d.kb_per_split);
             d.rc = d.splits > 1 ? std::max(1, d.bn / 32) : 0;
             if (d.tma) {   // pipeline depth from the real box sizes (SW128 needs 1 KB alignment)
-              d.st_boff = (int)rup(d.a_bytes, 1024);
+              d.st_boff = d.tma == 2 ? 16 * 1024 : (int)rup(d.a_bytes, 1024);
               d.st_bytes = d.st_boff + (int)rup(d.bn * 128, 1024);
               d.nst = std::min(MT_MAXST, MT_PIPE_BYTES / d.st_bytes);
             } else {
@@ -441,7 +462,7 @@ static mt_status plan_graphs(mt_ctx *c) {
               d.nst = MT_STAGES;
             }
             d.tiles = tmn * d.splits + tmn * d.rc;
-            wp.mode = d.tma ? 5 : 1;
+            wp.mode = d.tma == 1 ? 5 : 1;
             wp.bytes = (int64_t)d.tiles_n * d.bn * d.Kpad * 2;
             if (d.splits > 1) {
               d.cnt_off = split_cnt;
@@ -664,7 +685,7 @@ static RunArgs base_args(mt_ctx *c, const float *const *inputs, float *const *ou
     a.in_prec[t] = g.precision;
     // shared input: pack once per distinct (pointer, shape, precision)
     int src = t;
-    for (int u = 0; u < t; ++u) {
+    for (int u = 0; u < t && !c->T[t].tma_input; ++u) {
       const mt_graph &h = c->T[u].g;
       if (inputs && inputs[u] == inputs[t] && h.batch == g.batch && h.in_c == g.in_c &&
           h.in_h == g.in_h && h.in_w == g.in_w && h.precision == g.precision) { src = u; break; }
@@ -730,11 +751,13 @@ static mt_status make_conv_tmaps(mt_ctx *c, const OpDesc &o, const HostOp &h, ch
   cuuint64_t gdim[4] = {(cuuint64_t)o.C, (cuuint64_t)o.W, (cuuint64_t)o.H, (cuuint64_t)o.N};
   cuuint64_t gstr[3] = {(cuuint64_t)o.in_cs * es, (cuuint64_t)o.W * o.in_cs * es,
                         (cuuint64_t)o.H * o.W * o.in_cs * es};
-  cuuint32_t box[4] = {64, (cuuint32_t)(o.Wo * o.sw), (cuuint32_t)(o.blk_rows * o.sh), 1};
+  const bool small = o.tma == 2;   // 8-channel rows of 16 bytes, no swizzle
+  cuuint32_t box[4] = {small ? 8u : 64u, (cuuint32_t)(o.Wo * o.sw), (cuuint32_t)(o.blk_rows * o.sh), 1};
   cuuint32_t estr[4] = {1, (cuuint32_t)o.sw, (cuuint32_t)o.sh, 1};
-  void *base = (void *)(o.in + (uint64_t)o.in_co * es);
+  void *base = (o.flags & OPF_GRAPH_IN) ? (void *)(c->ws + c->lay.packed_off[o.tenant])
+                                        : (void *)(o.in + (uint64_t)o.in_co * es);
   CUresult r = enc(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, gdim, gstr, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, small ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char m[160];

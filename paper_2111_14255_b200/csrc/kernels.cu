@@ -128,6 +128,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// waiting warps that are not on the tile's critical issue path back off between probes so they
+// do not take issue slots from the TMA-producer / MMA lanes
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) __nanosleep(64);
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -187,6 +192,16 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   d |= (uint64_t)1 << 46;                      // descriptor version (sm_100)
   d |= (uint64_t)2 << 61;                      // SWIZZLE_128B
   return d;
+}
+// UMMA descriptor, K-major, no swizzle ("interleave"): 8-row x 16-byte core matrices, lbo = byte
+// distance between the two 16-byte K chunks of one MMA, sbo = distance between 8-row groups
+__device__ __forceinline__ uint64_t sdesc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;   // layout type 0 = SWIZZLE_NONE
 }
 // instruction descriptor kind::f16: D f32, A/B bf16, both K-major, M = 128, N = n
 __device__ __forceinline__ uint32_t idesc_bf16(int n) {
@@ -421,66 +436,96 @@ __device__ void conv_tc_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaSh
                      (uint32_t)(ct.nk - d.nst) * MT_BK * 2);
 }
 
-// TMA mainloop: thread 0 = producer (A boxes, and B beyond the prefetched stages), thread 32 =
-// MMA issuer (UMMA 128 x bn x 16 from the two SW128 tiles of a stage; commit frees the stage),
-// everyone else waits for the accumulator.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n\t.reg .pred q;\n\telect.sync _|q, 0xffffffff;\n\tselp.u32 %0, 1, 0, q;\n\t}" : "=r"(p));
+  return p != 0;
+}
+
+// TMA mainloop.  Warp 0 = producer (A boxes, and B beyond the prefetched stages), warp 1 = MMA
+// issuer (UMMA 128 x bn x 16 from a stage's two tiles; commit frees the stage); both loops run
+// warp-wide with one elected lane issuing, descriptors are precomputed and advanced by adds.
+// Everyone else waits for the accumulator.
 __device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const ConvTile &ct, uint8_t *smem,
                                                      CtaShared &sh, const PipeState &ps) {
-  const int tid = threadIdx.x;
+  const int warp = threadIdx.x >> 5;
   const uint32_t s0 = smem_u32(smem);
   const uint32_t bar_full0 = smem_u32(&sh.bar_full[0]);
   const uint32_t bar_empty0 = smem_u32(&sh.bar_empty[0]);
   const uint32_t bar_accf = smem_u32(&sh.bar_accf);
-  const int nst = d.nst;
-  // the role lanes (producer = lane 0 of warp 0, MMA issuer = lane 0 of warp 1) must not share
-  // their warp with lanes spinning on an mbarrier: the siblings park on __syncwarp instead
-  if (tid == 0) {
-    // incremental stage / tap / channel-block counters (no divisions in the issue loop)
+  const int nst = d.nst, nk = ct.nk, st_bytes = d.st_bytes, st_boff = d.st_boff;
+  if (warp == 0) {
     const uint32_t txb = (uint32_t)(d.a_bytes + d.bn * 128);
-    const int kb0 = ct.kb0;
-    int tap = kb0 / d.cblks, cb = kb0 - tap * d.cblks;
-    int rr = tap / d.kw, ss = tap - rr * d.kw;
+    const uint64_t tmap_a = d.tmap_a, tmap_b = d.tmap_b;
+    const int kb0 = ct.kb0, cblks = d.cblks, kw = d.kw, pw = d.pw, n0 = ct.n0, img = ct.img;
+    const int small = d.tma == 2, ntap = d.kh * d.kw;
+    int tap = kb0 / cblks, cb = kb0 - tap * cblks;
+    int rr = tap / kw, ss = tap - rr * kw;
     const int hbase = ct.ho0 * d.sh - d.ph;
+    const uint32_t eph = ps.eph;
     int s = 0, j = 0;
     uint32_t st = s0;
-    for (int i = 0; i < ct.nk; ++i) {
-      if (j > 0) {
-        mbar_wait(bar_empty0 + 8 * s, stage_par(ps.eph, s, j - 1));
-        mbar_expect_tx(bar_full0 + 8 * s, txb);
-        tma_load_2d(st + d.st_boff, d.tmap_b, bar_full0 + 8 * s, (kb0 + i) * MT_BK, ct.n0);
+    for (int i = 0; i < nk; ++i) {
+      if (j > 0) mbar_wait(bar_empty0 + 8 * s, ((eph >> s) & 1u) ^ (uint32_t)((j - 1) & 1));
+      if (elect_one()) {
+        const uint32_t bar = bar_full0 + 8 * s;
+        if (j > 0) {
+          mbar_expect_tx(bar, txb);
+          tma_load_2d(st + st_boff, tmap_b, bar, (kb0 + i) * MT_BK, n0);
+        }
+        if (small) {   // 8 taps x 8 channels: one 16-byte-row box per tap, 2 KB apart
+          int t8 = (kb0 + i) * 8;
+          for (int tt = 0; tt < 8; ++tt, ++t8) {
+            const int r2 = t8 / kw, s2 = t8 - r2 * kw;
+            const bool v = t8 < ntap;   // missing taps: an out-of-range box is zero-filled
+            tma_load_4d(st + tt * 2048, tmap_a, bar, 0, v ? s2 - pw : -(1 << 20), v ? hbase + r2 : 0, img);
+          }
+        } else {
+          tma_load_4d(st, tmap_a, bar, cb * 64, ss - pw, hbase + rr, img);
+        }
       }
-      tma_load_4d(st, d.tmap_a, bar_full0 + 8 * s, cb * 64, ss - d.pw, hbase + rr, ct.img);
-      if (i == 3) sh.t_is[0] = gtimer();
-      if (++cb == d.cblks) {
+      __syncwarp();
+      if (++cb == cblks) {
         cb = 0;
-        if (++ss == d.kw) { ss = 0; ++rr; }
+        if (++ss == kw) { ss = 0; ++rr; }
       }
-      st += d.st_bytes;
+      st += st_bytes;
       if (++s == nst) { s = 0; ++j; st = s0; }
     }
-    sh.t_aissue = gtimer();
-  } else if (tid == 32) {
+  } else if (warp == 1) {
     const uint32_t idesc = idesc_bf16(d.bn);
     const uint32_t tmem = sh.tmem_base;
+    const uint32_t fph = ps.fph;
+    const bool small = d.tma == 2;
+    // descriptors of stage 0; a stage advances the start-address field by st_bytes/16, one MMA K
+    // step by 32 B (SW128: +2) or 2 x 2 KB (no swizzle: +256)
+    const uint64_t ad0 = small ? sdesc_noswz(s0, 2048, 128) : sdesc_sw128(s0);
+    const uint64_t bd0 = sdesc_sw128(s0 + st_boff);
+    const uint64_t a_k = small ? 256 : 2, st16 = (uint64_t)(st_bytes >> 4);
+    uint64_t ad = ad0, bd = bd0;
     int s = 0, j = 0;
-    uint32_t ab = s0;
-    for (int i = 0; i < ct.nk; ++i) {
-      mbar_wait(bar_full0 + 8 * s, stage_par(ps.fph, s, j));
-      if (i == 0) sh.t_first = gtimer();
-      if (i == 12) sh.t_kb[3] = gtimer();
+    for (int i = 0; i < nk; ++i) {
+      mbar_wait(bar_full0 + 8 * s, ((fph >> s) & 1u) ^ (uint32_t)(j & 1));
       tc_fence_after();
-      const uint32_t bb = ab + d.st_boff;
-#pragma unroll
-      for (int kk = 0; kk < MT_BK / 16; ++kk)
-        tc_mma(tmem, sdesc_sw128(ab + kk * 32), sdesc_sw128(bb + kk * 32), idesc, (i > 0 || kk > 0) ? 1u : 0u);
-      tc_commit(bar_empty0 + 8 * s);
-      ab += d.st_bytes;
-      if (++s == nst) { s = 0; ++j; ab = s0; }
+      if (elect_one()) {
+        if (i == 0) sh.t_first = gtimer();
+        tc_mma(tmem, ad, bd, idesc, i > 0 ? 1u : 0u);
+        tc_mma(tmem, ad + a_k, bd + 2, idesc, 1u);
+        tc_mma(tmem, ad + 2 * a_k, bd + 4, idesc, 1u);
+        tc_mma(tmem, ad + 3 * a_k, bd + 6, idesc, 1u);
+        tc_commit(bar_empty0 + 8 * s);
+      }
+      __syncwarp();
+      ad += st16;
+      bd += st16;
+      if (++s == nst) { s = 0; ++j; ad = ad0; bd = bd0; }
     }
-    tc_commit(bar_accf);
-    sh.t_lastmma = gtimer();
+    if (elect_one()) {
+      tc_commit(bar_accf);
+      sh.t_lastmma = gtimer();
+    }
+    __syncwarp();
   }
-  if (tid < 64) __syncwarp();
 }
 
 // cp.async mainloop (small-channel convs, e.g. the 3->8-padded stems): all threads gather im2col
@@ -675,7 +720,8 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
       }
     }
   }
-  mbar_wait(bar_accf, ps.acc_phase);
+  if (tid < 64) mbar_wait(bar_accf, ps.acc_phase);
+  else mbar_wait_backoff(bar_accf, ps.acc_phase);
   ps.acc_phase ^= 1;
   tc_fence_after();
   if (tid == 0) sh.t_mma = gtimer();

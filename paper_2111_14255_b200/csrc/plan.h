@@ -16,6 +16,7 @@ struct Tenant {
   int L = 0;          // number of ops
   int op_base = 0;    // global id of op 0
   int cpad = 8;       // stored channels of the packed graph input
+  bool tma_input = false;   // a TMA conv reads the packed input: keep the tenant's own pack slot
 };
 
 struct Buf {          // one activation buffer (NHWC), possibly shared by a concat group

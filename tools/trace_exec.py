@@ -35,6 +35,14 @@ if a.synthetic and a.synthetic.startswith("pw:"):
         x = b.conv(x, ci, 1, 1, 0)
     b.gap(x)
     g = [b.build()]
+elif a.synthetic == "stempool":
+    b = zoo.GraphBuilder("tinyA", 1, 3, 224, 224, zoo.PREC_BF16, seed=0)
+    x = b.conv(-1, 64, 7, 2, 3)
+    for i in range(4):
+        x = b.maxpool(x, 3, 1, 1)
+    x = b.maxpool(x, 3, 2, 1)
+    b.gap(x)
+    g = [b.build()]
 elif a.synthetic:
     b = zoo.GraphBuilder("tinyA", 1, 384, 14, 14, zoo.PREC_BF16, seed=0)
     x = b.conv(-1, 384, 1, 1, 0)
