@@ -291,12 +291,22 @@ def main():
         dt = maxall(time.perf_counter() - t0)
         lat_p = lat_all[st_all == 0]
         st_p = st_all
+        # Alg.1 coordinate descent on the same mix (P=3, R=1, M=8), rank 0's GPU
+        search_line = None
+        if rank == 0:
+            from paper_2111_14255_b200 import search as S
+            t1 = time.perf_counter()
+            cdr = S.coordinate_descent(pfn, PL, P=3, rounds=1, m=8, seed=14255)
+            search_line = {"algorithm": "coordinate descent (Alg.1), P=3 R=1 M=8", "evaluations": cdr.evaluations,
+                           "best_us": cdr.best_lat, "start_us": cdr.records[0][1],
+                           "wall_s": time.perf_counter() - t1}
         prof_line = {"config": args.profile_config, "candidates": args.n_cand, "warmup": 2, "iters": 10,
                      "schedules_per_s": args.n_cand / dt, "wall_s": dt,
                      "feasible": int((st_p == 0).sum()),
                      "best_us": float(np.nanmin(lat_p)) if len(lat_p) else None,
                      "median_us": float(np.nanmedian(lat_p)) if len(lat_p) else None,
-                     "gather": "NCCL all_gather of per-rank latencies" if ws > 1 else "none (1 GPU)"}
+                     "gather": "NCCL all_gather of per-rank latencies" if ws > 1 else "none (1 GPU)",
+                     "search": search_line}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:

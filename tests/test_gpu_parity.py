@@ -193,3 +193,19 @@ def test_unfused_ops_and_pool_variants():
         errs = teacher_forced_errors(m, x, 0)
         assert max(errs) <= tol, errs
         assert rel_err(m.outputs_numpy()[0], fw.forward(g, x, mode)) <= tol
+
+
+def test_search_drivers_on_gpu_profiler():
+    """f1: coordinate descent (Alg.1) and random search through mt_profile_batch; the returned best
+    is the best record, and it is never worse than the search's own starting point"""
+    from paper_2111_14255_b200 import search
+    m = mix_for("c2")
+    L = [g.n_ops for g in m.graphs]
+    pf = lambda cs: m.ctx.profile_batch_pointers(cs, m.in_ptrs, m.out_ptrs, warmup=1, iters=3)
+    cd = search.coordinate_descent(pf, L, P=2, rounds=1, m=4, seed=0)
+    assert cd.evaluations == 1 + 1 * 2 * 4
+    assert cd.best_lat <= cd.records[0][1] and cd.best_lat == cd.sorted_records()[0][1]
+    rs = search.random_search(pf, L, 12, p_max=3, seed=0)
+    assert rs.best_rho is not None and np.isfinite(rs.best_lat)
+    m.ctx.set_schedule_pointers(cd.best_rho)
+    m.run()

@@ -1,0 +1,52 @@
+"""Search drivers (f1) with a synthetic cost on CPU: Alg.1 bookkeeping, determinism, filtering of
+infeasible candidates, and optimality on an exhaustively enumerable space (oracle enumeration)."""
+import numpy as np
+import pytest
+
+from oracle import ir
+from paper_2111_14255_b200 import search
+
+
+def _cost(lengths):
+    """synthetic latency: per stage, the longest slice + 1 (barrier); infeasible -> status 2"""
+    def fn(cands):
+        lat, st = [], []
+        for rho in cands:
+            status, ranges = ir.T(lengths, rho)
+            if status[0] != ir.E_OK:
+                lat.append(np.nan)
+                st.append(2)
+                continue
+            lat.append(sum(max(e - b for b, e in stage) + 1.0 for stage in ranges))
+            st.append(0)
+        return np.array(lat, np.float32), np.array(st, np.int32)
+    return fn
+
+
+def test_coordinate_descent_evaluation_count_and_records():
+    lengths = (5, 4, 6)
+    res = search.coordinate_descent(_cost(lengths), lengths, P=2, rounds=2, m=10, seed=1)
+    assert res.evaluations == 1 + 2 * 3 * 10          # R=2, N=3, M=10 -> 60 (+1)
+    assert len(res.records) == res.evaluations
+    ok = res.sorted_records()
+    assert ok and ok[0][1] == res.best_lat and ok[0][0] == res.best_rho
+    assert all(r[2] != 0 for r in res.records if not np.isfinite(r[1]))
+
+
+def test_searches_deterministic_for_a_seed():
+    lengths = (4, 3)
+    a = search.coordinate_descent(_cost(lengths), lengths, P=2, rounds=2, m=6, seed=7)
+    b = search.coordinate_descent(_cost(lengths), lengths, P=2, rounds=2, m=6, seed=7)
+    key = lambda res: [(r, repr(l), s) for r, l, s in res.records]   # NaN-safe comparison
+    assert key(a) == key(b)
+    c = search.random_search(_cost(lengths), lengths, 50, p_max=3, seed=3)
+    d = search.random_search(_cost(lengths), lengths, 50, p_max=3, seed=3)
+    assert key(c) == key(d) and c.best_rho == d.best_rho
+
+
+@pytest.mark.parametrize("lengths", [(2, 2), (3, 2)])
+def test_random_search_reaches_exhaustive_optimum(lengths):
+    cost = _cost(lengths)
+    best = min(cost([ir.to_pointers(lengths, s)])[0][0] for s in ir.enumerate_schedules(lengths))
+    res = search.random_search(cost, lengths, 400, p_max=sum(lengths) - 1, seed=0)
+    assert res.best_lat == best
