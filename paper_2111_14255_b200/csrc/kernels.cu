@@ -37,6 +37,7 @@ struct CtaShared {
   int smem_cap;               // bytes of dynamic shared memory this kernel has (staging budget)
   unsigned long long t_pick, t_pick_next, t_deps, t_mma, t_run, t_first, t_lastmma, t_aissue;
   unsigned long long t_kb[4], t_is[1];
+  int *xrel;   // extra counter released with the tile (split-K partial arrival)
   int cur[MT_MAXT], end[MT_MAXT];
   uint32_t complete[64];      // bitset of ops observed fully complete (global op id < 2048)
   float esc[128], esh[128];   // epilogue scale / shift of the current conv tile's columns
@@ -78,6 +79,12 @@ __device__ __forceinline__ void st_release_u(unsigned *p, unsigned v) {
 }
 __device__ __forceinline__ void red_release_add(int *p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// release pattern (PTX memory model): one gpu-scope fence followed by relaxed reds -- every red
+// publishes the writes ordered before the fence, at the cost of a single MEMBAR.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void red_relaxed_add(int *p, int v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -232,6 +239,9 @@ __device__ __forceinline__ void ld8_cg(const float *p, float *v) {
 template <typename T> struct Raw8;
 template <> struct Raw8<bf16> { uint4 u; };
 template <> struct Raw8<float> { float4 a, b; };
+__device__ __forceinline__ uint32_t raw_word(const Raw8<bf16> &r) { return r.u.x; }
+__device__ __forceinline__ uint32_t raw_word(const Raw8<float> &r) { return __float_as_uint(r.a.x); }
+__shared__ unsigned long long sh_t_first_dw, sh_t_load_dw;   // trace stamps (dw tiles)
 __device__ __forceinline__ void ldraw_cg(const bf16 *p, Raw8<bf16> &r) {
   asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.u.x), "=r"(r.u.y), "=r"(r.u.z), "=r"(r.u.w) : "l"(p));
 }
@@ -736,6 +746,7 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
   if (S == 1) {
     if (hcols >= 32) {
       for (int cb = half * hcols; cb < (half + 1) * hcols; cb += 32) {
+        if (tid == 0 && cb == 0) sh.t_kb[0] = gtimer();
         // residual of these 32 columns requested before the TMEM drain (hides its L2 latency)
         uint4 rr[4] = {};
         const bool okrow = m >= 0;
@@ -746,6 +757,7 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
         }
         float v[32];
         tmem_ld32(tl + cb, v);
+        if (tid == 0 && cb == 0) sh.t_kb[1] = gtimer();
         if (okrow) {
           if ((d.flags & OPF_RES) && n0 + cb + 32 <= d.Co) {
 #pragma unroll
@@ -798,12 +810,13 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
           for (int e = 0; e < 8; ++e) __stcg(p + e * MT_BM, v[e]);
       }
     }
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) red_release_add(a.splitcnt + d.cnt_off + tmn, 1);
+    // published together with the tile's completion in run_stage (one fence for all counters)
+    if (tid == 0) sh.xrel = a.splitcnt + d.cnt_off + tmn;
   }
+  if (tid == 0) sh.t_kb[2] = gtimer();
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) sh.t_kb[3] = gtimer();
 }
 
 // ------------------------------------------------------------------------------------------
@@ -981,6 +994,7 @@ __device__ void dw3_tile(const RunArgs &a, const OpDesc &d, int tile, const uint
   const T *X = in_ptr<T>(a, d);
   cp_async_wait<0>();   // weights / scale / shift staged by tile_prefetch during the dependency wait
   __syncthreads();
+  if (threadIdx.x == 0) sh_t_first_dw = gtimer();
   const float *Wt = reinterpret_cast<const float *>(smem);
   const float *sc = Wt + 9 * d.C;
   const float *sf = Wt + 10 * d.C;
@@ -1016,6 +1030,7 @@ __device__ void dw3_tile(const RunArgs &a, const OpDesc &d, int tile, const uint
         xr[r][c] = ldraw_cg_pred(xb + (int64_t)(hi * W + wi) * cs, rok && wi >= 0 && wi < W);
       }
     }
+    if (threadIdx.x == 0 && it == 0) { const uint32_t u = raw_word(xr[2][NC - 1]); sh_t_load_dw = gtimer() + (u == 0x7fff1234u); }
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
       float2 w2[3][4];   // this kernel row's 3 taps (fp32 weights, [9][C])
@@ -1466,6 +1481,7 @@ __device__ __forceinline__ uint8_t *smem_base() {
 __device__ void cta_setup(CtaShared &sh, bool need_tmem) {
   const int tid = threadIdx.x;
   if (tid == 0) {
+    sh.xrel = nullptr;
     for (int s = 0; s < MT_MAXST; ++s) {
       mbar_init(smem_u32(&sh.bar_empty[s]), 1);
       mbar_init(smem_u32(&sh.bar_full[s]), 1);
@@ -1546,7 +1562,8 @@ __device__ __forceinline__ void trace_tile(const RunArgs &a, const CtaShared &sh
   e[8] = sh.t_first;      // MMA thread: first stage landed
   e[9] = sh.t_lastmma;    // MMA thread: last MMA issued
   e[10] = sh.t_aissue;    // producer: last A box issued
-  e[11] = sh.t_kb[0]; e[12] = sh.t_kb[1]; e[13] = sh.t_kb[2]; e[14] = sh.t_kb[3];   // stages 1,4,8,12 landed
+  e[11] = sh.t_kb[0]; e[12] = sh.t_kb[1]; e[13] = sh.t_kb[2]; e[14] = sh.t_kb[3];   // epilogue phases (TC)
+  if (!sh.t_kb[0]) { e[11] = sh_t_first_dw; e[12] = sh_t_load_dw; }                    // dw: staged, loads back
   e[15] = sh.t_is[0];     // producer: 4th A box issued
 }
 
@@ -1606,6 +1623,7 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
       sh.t_pick = sh.t_pick_next;
       sh.t_mma = sh.t_first = sh.t_lastmma = sh.t_aissue = 0;
       sh.t_kb[0] = sh.t_kb[1] = sh.t_kb[2] = sh.t_kb[3] = sh.t_is[0] = 0;
+      sh_t_first_dw = sh_t_load_dw = 0;
     }
     load_desc(sh, a.ops + op);
     __syncthreads();
@@ -1690,8 +1708,10 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
       sh.t_run = gtimer();
       const int b = tile_block(sh.d, my_tile, sh);
       const int boff = sh.d.blk_off;
-      if (b >= 0) red_release_add(a.blkcnt + boff + b, 1);
-      red_release_add(a.done + op, 1);
+      fence_acq_rel_gpu();
+      if (sh.xrel) { red_relaxed_add(sh.xrel, 1); sh.xrel = nullptr; }
+      if (b >= 0) red_relaxed_add(a.blkcnt + boff + b, 1);
+      red_relaxed_add(a.done + op, 1);
       if (a.trace) {
         sh.last = (int)(gtimer() - sh.t_run);
         trace_tile(a, sh, op, my_tile);
@@ -1754,6 +1774,11 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) op_kernel(RunArgs a, int op) {
     if (threadIdx.x == 0) sh.t_deps = gtimer();
     __syncthreads();
     run_tile(a, sh.d, t, smem, sh, ps);
+    if (threadIdx.x == 0 && sh.xrel) {   // split-K partial arrival (reduce tiles of this launch spin on it)
+      fence_acq_rel_gpu();
+      red_relaxed_add(sh.xrel, 1);
+      sh.xrel = nullptr;
+    }
     if (threadIdx.x == 0) trace_tile(a, sh, op, t);
   }
   cta_teardown(sh, tc);
@@ -1767,7 +1792,7 @@ __global__ void __launch_bounds__(MT_NTHREADS) op_kernel_small(RunArgs a, int op
   __shared__ __align__(16) CtaShared sh;
   PipeState ps{0u, 0u, 0u};
   load_desc(sh, a.ops + op);
-  if (threadIdx.x == 0) sh.smem_cap = SMALL_SMEM - 1024;
+  if (threadIdx.x == 0) { sh.smem_cap = SMALL_SMEM - 1024; sh.xrel = nullptr; }
   __syncthreads();
   for (int t = blockIdx.x; t < sh.d.tiles; t += gridDim.x) {
     if (threadIdx.x == 0) { sh.t_pick = gtimer(); sh.t_mma = 0; sh.home = -1; }
