@@ -70,7 +70,7 @@ def test_c1_schedule_invariance_sampled():
 
 
 # ---------------------------------------------------------------- bf16 tensor-core configs
-@pytest.mark.parametrize("config", ["c2", "c3", "c4", "c4b8"])
+@pytest.mark.parametrize("config", ["c2", "c3", "c4", "c4b8", "f2_models"])
 def test_end_to_end_vs_oracle(config):
     m = mix_for(config)
     L = [g.n_ops for g in m.graphs]
@@ -82,7 +82,7 @@ def test_end_to_end_vs_oracle(config):
         assert e_bf <= 1e-2, (g.name, e_bf)
 
 
-@pytest.mark.parametrize("config", ["c2", "c3", "c4", "c4b8"])
+@pytest.mark.parametrize("config", ["c2", "c3", "c4", "c4b8", "f2_models"])
 def test_teacher_forced_every_op(config):
     """every op (all 134 conv shapes, dw, pools, FC at b=1 and b=8, concat, residual) recomputed by
     the oracle from the GPU's own bf16 inputs, within 1e-2 of the op's output scale"""

@@ -22,12 +22,20 @@ CONFIGS = {
            zoo.PREC_BF16, "5-tenant mix b1"),
     "c4b8": (("resnet50", "inception_v3", "vgg16", "mobilenet_v2", "squeezenet1_0"), 8,
              zoo.PREC_BF16, "5-tenant mix b8"),
-    # paper zoo mixes (Table I / II) -- SURVEY §8(f) f2
+    # paper zoo mixes (Table I, Table II) -- SURVEY §8(f) f2
     "vgg_r18": (("vgg16", "resnet18"), 1, zoo.PREC_BF16, "Table I VGG+R18"),
-    "r18_r34_r50": (("resnet18", "resnet34", "resnet50"), 1, zoo.PREC_BF16, "Table I R18+R34+R50"),
+    "r18_r34": (("resnet18", "resnet34"), 1, zoo.PREC_BF16, "Table I R18+R34"),
+    "r34_r50": (("resnet34", "resnet50"), 1, zoo.PREC_BF16, "Table I R34+R50"),
+    "r50_r101": (("resnet50", "resnet101"), 1, zoo.PREC_BF16, "Table I R50+R101"),
+    "vgg_r18_r50": (("vgg16", "resnet18", "resnet50"), 1, zoo.PREC_BF16, "Table I/II VGG+R18+R50"),
+    "r18_r34_r50": (("resnet18", "resnet34", "resnet50"), 1, zoo.PREC_BF16, "Table I/II R18+R34+R50"),
     "zoo5": (("vgg16", "resnet18", "resnet34", "resnet50", "resnet101"), 1, zoo.PREC_BF16,
              "Table I VGG+R18+R34+R50+R101"),
     "alex_vgg_r18": (("alexnet", "vgg16", "resnet18"), 1, zoo.PREC_BF16, "Table II Alex+VGG+R18"),
+    "r18_r34_r101": (("resnet18", "resnet34", "resnet101"), 1, zoo.PREC_BF16, "Table II R18+R34+R101"),
+    "r18_r50_r101": (("resnet18", "resnet50", "resnet101"), 1, zoo.PREC_BF16, "Table II R18+R50+R101"),
+    # the f2 architectures not in configs 1-4, for per-op parity
+    "f2_models": (("alexnet", "resnet34", "resnet101"), 1, zoo.PREC_BF16, "AlexNet+R34+R101 (parity)"),
     # single tenants (profiling the per-op dependency chain)
     "mbv2": (("mobilenet_v2",), 1, zoo.PREC_BF16, "MobileNet-V2 alone"),
     "r18": (("resnet18",), 1, zoo.PREC_BF16, "ResNet-18 alone"),
