@@ -385,32 +385,35 @@ static mt_status plan_graphs(mt_ctx *c) {
             d.tiles_n = (int)cdiv(os.c, d.bn);
             // TMA mainloop: whole output rows per M tile; a K-block is one tap x 64 channels, loaded
             // as one 4-D box {64 ch, Wo*sw, R*sh, 1} with element strides {1, sw, sh, 1}
-            const int Rrows = std::min(os.h, 128 / std::max(os.w, 1));
-            if (!iv.graph_in && d.C >= 16 && os.w <= 128 && os.w * n.sw <= 256 && Rrows >= 1 &&
-                Rrows * n.sh <= 256) {
+            // rows wider than 128 pixels: nseg column segments of seg_w pixels, one row per tile
+            const int nseg = (int)cdiv(std::max(os.w, 1), 128);
+            const int seg_w = (int)cdiv(std::max(os.w, 1), nseg);
+            const int Rrows = std::min(os.h, 128 / seg_w);
+            const bool geo_ok = seg_w * n.sw <= 256 && Rrows >= 1 && Rrows * n.sh <= 256;
+            if (!iv.graph_in && d.C >= 16 && geo_ok) {
               d.tma = 1;
-              d.blk_rows = Rrows;
-              d.blk_tpi = (int)cdiv(os.h, Rrows);
-              d.tiles_m = g.batch * d.blk_tpi;
               d.cblks = (int)cdiv(d.C, 64);
               d.nkb = n.kh * n.kw * d.cblks;
               d.Kpad = d.nkb * MT_BK;
               d.K = d.Kpad;
-              d.a_bytes = Rrows * os.w * 128;
-            } else if (d.C == 8 && os.w <= 128 && os.w * n.sw <= 256 && Rrows >= 1 && Rrows * n.sh <= 256 &&
-                       (!iv.graph_in || g.in_c <= 8)) {
+              d.a_bytes = Rrows * seg_w * 128;
+            } else if (d.C == 8 && geo_ok && (!iv.graph_in || g.in_c <= 8)) {
               // 8-channel input (the padded 3-channel stems): one 16-byte-row box per filter tap,
               // 8 taps per K-block, canonical no-swizzle K-major layout
               d.tma = 2;
-              d.blk_rows = Rrows;
-              d.blk_tpi = (int)cdiv(os.h, Rrows);
-              d.tiles_m = g.batch * d.blk_tpi;
               d.cblks = 1;
               d.K = n.kh * n.kw * 8;
               d.Kpad = (int)rup(d.K, MT_BK);
               d.nkb = d.Kpad / MT_BK;
-              d.a_bytes = 8 * Rrows * os.w * 16;
+              d.a_bytes = 8 * Rrows * seg_w * 16;
               if (iv.graph_in) tn.tma_input = true;
+            }
+            if (d.tma) {
+              d.nseg = nseg;
+              d.seg_w = seg_w;
+              d.blk_rows = Rrows;
+              d.blk_tpi = (int)cdiv(os.h, Rrows);
+              d.tiles_m = g.batch * d.blk_tpi * nseg;
             } else {
               d.K = n.kh * n.kw * d.C;
               d.Kpad = (int)rup(d.K, MT_BK);
@@ -428,7 +431,7 @@ static mt_status plan_graphs(mt_ctx *c) {
               double best = 1e30;
               const int bn_max = d.bn;
               const double a_kb = d.tma ? (double)d.a_bytes : 16384.0;   // bytes of A per k-block
-              const double rows = d.tma ? (double)d.blk_rows * os.w : 128.0;
+              const double rows = d.tma ? (double)d.blk_rows * d.seg_w : 128.0;
               for (int bn = bn_max; bn >= 32 || bn == bn_max; bn >>= 1) {
                 const int64_t tn = cdiv(os.c, bn), tmn_c = (int64_t)d.tiles_m * tn;
                 const double t_kb = std::max(0.13 * bn / 128.0, (a_kb + bn * 128.0) / 160000.0);
@@ -525,7 +528,7 @@ static mt_status plan_graphs(mt_ctx *c) {
     switch (d.tk) {
       case TK_CONV_TC:   // (blk_rows for TMA); split-K: the reduce tiles complete the block
         d.pix_blk = MT_BM;
-        d.blk_need = d.tiles_n * (d.splits > 1 ? d.rc : 1);
+        d.blk_need = d.tiles_n * (d.splits > 1 ? d.rc : 1) * (d.tma ? d.nseg : 1);
         break;
       case TK_CONV_SIMT: d.pix_blk = MT_SIMT_BM; d.blk_need = d.tiles_n; break;
       case TK_GAP: d.pix_blk = 1; d.blk_need = (int)cdiv(d.Co / 8, 32); break;
@@ -752,7 +755,7 @@ static mt_status make_conv_tmaps(mt_ctx *c, const OpDesc &o, const HostOp &h, ch
   cuuint64_t gstr[3] = {(cuuint64_t)o.in_cs * es, (cuuint64_t)o.W * o.in_cs * es,
                         (cuuint64_t)o.H * o.W * o.in_cs * es};
   const bool small = o.tma == 2;   // 8-channel rows of 16 bytes, no swizzle
-  cuuint32_t box[4] = {small ? 8u : 64u, (cuuint32_t)(o.Wo * o.sw), (cuuint32_t)(o.blk_rows * o.sh), 1};
+  cuuint32_t box[4] = {small ? 8u : 64u, (cuuint32_t)(o.seg_w * o.sw), (cuuint32_t)(o.blk_rows * o.sh), 1};
   cuuint32_t estr[4] = {1, (cuuint32_t)o.sw, (cuuint32_t)o.sh, 1};
   void *base = (o.flags & OPF_GRAPH_IN) ? (void *)(c->ws + c->lay.packed_off[o.tenant])
                                         : (void *)(o.in + (uint64_t)o.in_co * es);

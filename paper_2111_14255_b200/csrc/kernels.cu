@@ -357,7 +357,7 @@ __device__ __forceinline__ void store_out8(const RunArgs &a, const OpDesc &d, in
 // ------------------------------------------------------------------------------------------
 struct ConvTile {
   int tmn, ks, mt, m0, n0, kb0, nk;
-  int img, ho0;   // TMA path: image and first output row of the M tile
+  int img, ho0, wo0;   // TMA path: image, first output row and first column of the M tile
 };
 __device__ __forceinline__ ConvTile conv_tile_coords(const OpDesc &d, int tile) {
   ConvTile c;
@@ -371,30 +371,27 @@ __device__ __forceinline__ ConvTile conv_tile_coords(const OpDesc &d, int tile) 
   c.kb0 = c.ks * d.kb_per_split;
   c.nk = min(d.nkb, c.kb0 + d.kb_per_split) - c.kb0;
   if (d.tma) {
-    c.img = c.mt / d.blk_tpi;
-    c.ho0 = (c.mt - c.img * d.blk_tpi) * d.blk_rows;
+    const int rg = c.mt / d.nseg, seg = c.mt - rg * d.nseg;
+    c.img = rg / d.blk_tpi;
+    c.ho0 = (rg - c.img * d.blk_tpi) * d.blk_rows;
+    c.wo0 = seg * d.seg_w;
   } else {
     c.img = 0;
     c.ho0 = 0;
+    c.wo0 = 0;
   }
   return c;
 }
 // output pixel of accumulator row r (TMEM lane), or -1 if the row is padding
 __device__ __forceinline__ int conv_row_pixel(const OpDesc &d, const ConvTile &c, int r) {
   if (d.tma) {
-    const int hl = r / d.Wo;
-    const int ho = c.ho0 + hl;
-    if (hl >= d.blk_rows || ho >= d.Ho) return -1;
-    return (c.img * d.Ho + ho) * d.Wo + (r - hl * d.Wo);
+    const int hl = r / d.seg_w;
+    const int ho = c.ho0 + hl, wo = c.wo0 + (r - hl * d.seg_w);
+    if (hl >= d.blk_rows || ho >= d.Ho || wo >= d.Wo) return -1;
+    return (c.img * d.Ho + ho) * d.Wo + wo;
   }
   const int m = c.m0 + r;
   return m < d.M ? m : -1;
-}
-// TMA: issue the A box of k-block kb (one tap, 64 channels) for this M tile
-__device__ __forceinline__ void tma_issue_a(const OpDesc &d, const ConvTile &c, int kb, uint32_t dst, uint32_t bar) {
-  const int tap = kb / d.cblks, cb = kb - tap * d.cblks;
-  const int r = tap / d.kw, s = tap - r * d.kw;
-  tma_load_4d(dst, d.tmap_a, bar, cb * 64, s - d.pw, c.ho0 * d.sh + r - d.ph, c.img);
 }
 
 // parity helpers: k-block i of a tile uses stage i % nst; its j-th use (j = i / nst) of the stage
@@ -471,7 +468,7 @@ __device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const Conv
     const int small = d.tma == 2, ntap = d.kh * d.kw;
     int tap = kb0 / cblks, cb = kb0 - tap * cblks;
     int rr = tap / kw, ss = tap - rr * kw;
-    const int hbase = ct.ho0 * d.sh - d.ph;
+    const int hbase = ct.ho0 * d.sh - d.ph, wbase = ct.wo0 * d.sw - pw;
     const uint32_t eph = ps.eph;
     int s = 0, j = 0;
     uint32_t st = s0;
@@ -488,10 +485,10 @@ __device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const Conv
           for (int tt = 0; tt < 8; ++tt, ++t8) {
             const int r2 = t8 / kw, s2 = t8 - r2 * kw;
             const bool v = t8 < ntap;   // missing taps: an out-of-range box is zero-filled
-            tma_load_4d(st + tt * 2048, tmap_a, bar, 0, v ? s2 - pw : -(1 << 20), v ? hbase + r2 : 0, img);
+            tma_load_4d(st + tt * 2048, tmap_a, bar, 0, v ? wbase + s2 : -(1 << 20), v ? hbase + r2 : 0, img);
           }
         } else {
-          tma_load_4d(st, tmap_a, bar, cb * 64, ss - pw, hbase + rr, img);
+          tma_load_4d(st, tmap_a, bar, cb * 64, wbase + ss, hbase + rr, img);
         }
       }
       __syncwarp();
@@ -656,7 +653,7 @@ __device__ void conv_reduce_tile(const RunArgs &a, const OpDesc &d, int rtile, u
   }
   // valid accumulator rows form a prefix of the 128 TMEM lanes
   int nv;
-  if (d.tma) nv = min(d.blk_rows, d.Ho - ct.ho0) * d.Wo;
+  if (d.tma) nv = d.nseg > 1 ? min(d.seg_w, d.Wo - ct.wo0) : min(d.blk_rows, d.Ho - ct.ho0) * d.Wo;
   else nv = min(MT_BM, d.M - ct.m0);
   const int c0 = rc * 32;
   const int ncol = min(32, d.bn - c0);
@@ -1381,10 +1378,11 @@ __device__ __forceinline__ void tile_out_range(const OpDesc &d, int tile, int64_
       if (d.splits > 1 && tile >= d.tiles_m * d.tiles_n * d.splits)   // reduce tile -> its (M,N) tile
         tile = ((tile - d.tiles_m * d.tiles_n * d.splits) / d.rc) * d.splits;
       if (d.tma) {
-        const int mt = (tile / d.splits) / d.tiles_n, img = mt / d.blk_tpi;
-        const int ho0 = (mt - img * d.blk_tpi) * d.blk_rows;
-        p0 = ((int64_t)img * d.Ho + ho0) * d.Wo;
-        p1 = ((int64_t)img * d.Ho + min(d.Ho, ho0 + d.blk_rows)) * d.Wo;
+        const int mt = (tile / d.splits) / d.tiles_n, rg = mt / d.nseg, seg = mt - rg * d.nseg;
+        const int img = rg / d.blk_tpi, ho0 = (rg - img * d.blk_tpi) * d.blk_rows;
+        p0 = ((int64_t)img * d.Ho + ho0) * d.Wo + seg * d.seg_w;
+        p1 = d.nseg > 1 ? p0 + min(d.seg_w, d.Wo - seg * d.seg_w)
+                        : ((int64_t)img * d.Ho + min(d.Ho, ho0 + d.blk_rows)) * d.Wo;
       } else {
         p0 = (int64_t)((tile / d.splits) / d.tiles_n) * MT_BM;
         p1 = p0 + MT_BM;
@@ -1414,10 +1412,11 @@ __device__ __forceinline__ void tile_in_range(const OpDesc &d, int64_t p0, int64
 // completion block a finished tile contributes to (-1: none, e.g. a non-final split-K part)
 __device__ __forceinline__ int tile_block(const OpDesc &d, int tile, const CtaShared &sh) {
   switch (d.tk) {
-    case TK_CONV_TC: {
-      if (d.splits == 1) return tile / d.tiles_n;
+    case TK_CONV_TC: {   // block = M tile (TMA: row group, i.e. all column segments of it)
+      const int ns = d.tma ? d.nseg : 1;
+      if (d.splits == 1) return tile / d.tiles_n / ns;
       const int nct = d.tiles_m * d.tiles_n * d.splits;
-      return tile >= nct ? ((tile - nct) / d.rc) / d.tiles_n : -1;   // only reduce tiles complete
+      return tile >= nct ? ((tile - nct) / d.rc) / d.tiles_n / ns : -1;   // only reduce tiles complete
     }
     case TK_CONV_SIMT: return tile / d.tiles_n;
     case TK_GAP: return tile / ((d.Co / 8 + 31) / 32);

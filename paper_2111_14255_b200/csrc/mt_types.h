@@ -54,6 +54,9 @@ struct OpDesc {
   int32_t blk_rows;                 // >0: blocks are whole-row M-tiles (TMA conv): block of pixel p =
                                     //     n * blk_tpi + ho / blk_rows
   int32_t blk_tpi;                  // tiles (blocks) per image for blk_rows > 0
+  int32_t nseg, seg_w;              // TMA: an output row wider than 128 is split into nseg column
+                                    //     segments of seg_w pixels (one M tile each, blk_rows = 1);
+                                    //     the nseg segment tiles of a row complete one block
   int32_t tma;                      // 1: TMA mainloop (whole-row M tiles, K-block = tap x 64 ch)
   int32_t cblks;                    // TMA: 64-channel blocks per tap
   int32_t a_bytes;                  // TMA: bytes of one A box (rows * Wo * 128)

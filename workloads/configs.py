@@ -40,6 +40,8 @@ CONFIGS = {
     "mbv2": (("mobilenet_v2",), 1, zoo.PREC_BF16, "MobileNet-V2 alone"),
     "r18": (("resnet18",), 1, zoo.PREC_BF16, "ResNet-18 alone"),
     "r50": (("resnet50",), 1, zoo.PREC_BF16, "ResNet-50 alone"),
+    "vgg": (("vgg16",), 1, zoo.PREC_BF16, "VGG-16 alone"),
+    "vgg_b8": (("vgg16",), 8, zoo.PREC_BF16, "VGG-16 alone, batch 8"),
 }
 
 
