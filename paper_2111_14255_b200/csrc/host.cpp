@@ -501,6 +501,44 @@ static mt_status plan_graphs(mt_ctx *c) {
           if (!(iv.graph_in || (iv.cs == iv.C && iv.co == 0)))
             return fail(c, MT_ERR_ARG, "FC input must be a contiguous tensor");
           d.K = ins.h * ins.w * d.C;
+          if (bf16 && !iv.graph_in && d.K % 8 == 0 &&
+              (g.batch > 1 || (int64_t)os.c * d.K * 2 >= ((int64_t)8 << 20))) {
+            // tensor-core FC (swap-AB): D[128 features][bn batch] = W[128][K] . X[bn][K]^T on
+            // tcgen05, W and X streamed by TMA (2-D boxes, SW128), split-K over the SMs; used when
+            // the weight stream is large (bandwidth-bound GEMV) or the batch makes CUDA-core FMAs
+            // the bottleneck.  DESIGN.md section 5.
+            d.tma = 3;
+            d.tk = TK_CONV_TC;
+            d.kh = d.kw = 1;
+            d.cblks = 1;
+            d.M = os.c;
+            d.bn = g.batch <= 16 ? 16 : 32;
+            d.tiles_n = (int)cdiv(g.batch, d.bn);
+            d.tiles_m = (int)cdiv(os.c, MT_BM);
+            d.nkb = (int)cdiv(d.K, MT_BK);
+            d.Kpad = d.nkb * MT_BK;
+            d.a_bytes = MT_BM * 128;
+            const int64_t tmn = (int64_t)d.tiles_m * d.tiles_n;
+            // one wave: every compute tile of the op can be resident at once (148 SMs)
+            const int want = (int)std::max<int64_t>(1, std::min<int64_t>(d.nkb / 8, 148 / tmn));
+            d.kb_per_split = (int)cdiv(d.nkb, want);
+            d.splits = (int)cdiv(d.nkb, d.kb_per_split);
+            d.rc = d.splits > 1 ? 1 : 0;
+            d.st_boff = d.a_bytes;
+            d.st_bytes = d.st_boff + (int)rup(d.bn * 128, 1024);
+            d.nst = std::min(MT_MAXST, MT_PIPE_BYTES / d.st_bytes);
+            d.tiles = (int)(tmn * d.splits + tmn * d.rc);
+            if (d.splits > 1) {
+              d.cnt_off = split_cnt;
+              split_cnt += (int)tmn;
+              h.ws_off = pbytes;
+              h.ws_bytes = tmn * d.splits * MT_BM * d.bn * 4;
+              pbytes += rup(h.ws_bytes, 256);
+            }
+            wp.mode = 4;
+            wp.bytes = (int64_t)os.c * d.K * eb;
+            break;
+          }
           d.tiles = (int)(cdiv(os.c, MT_FC_ROWS) * cdiv(g.batch, MT_FC_BATCH));
           wp.mode = 4;
           wp.bytes = (int64_t)os.c * d.K * eb;
@@ -527,6 +565,11 @@ static mt_status plan_graphs(mt_ctx *c) {
     const int64_t npix = (int64_t)d.N * d.Ho * d.Wo;
     switch (d.tk) {
       case TK_CONV_TC:   // (blk_rows for TMA); split-K: the reduce tiles complete the block
+        if (d.tma == 3) {   // tensor-core FC: block = one batch tile (bn images), all feature tiles
+          d.pix_blk = d.bn;
+          d.blk_need = d.tiles_m * (d.splits > 1 ? d.rc : 1);
+          break;
+        }
         d.pix_blk = MT_BM;
         d.blk_need = d.tiles_n * (d.splits > 1 ? d.rc : 1) * (d.tma ? d.nseg : 1);
         break;
@@ -751,6 +794,22 @@ static mt_status make_conv_tmaps(mt_ctx *c, const OpDesc &o, const HostOp &h, ch
   if (!enc) return fail(c, MT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   alignas(64) CUtensorMap ma, mb;
   const cuuint64_t es = 2;
+  if (o.tma == 3) {   // tensor-core FC: A = packed weights {K, Co} box {64, 128}; B = input {K, N} box {64, bn}
+    cuuint64_t adim[2] = {(cuuint64_t)o.K, (cuuint64_t)o.Co}, astr[1] = {(cuuint64_t)o.K * es};
+    cuuint64_t bdim[2] = {(cuuint64_t)o.K, (cuuint64_t)o.N}, bstr[1] = {(cuuint64_t)o.K * es};
+    cuuint32_t abox[2] = {64, (cuuint32_t)MT_BM}, bbox[2] = {64, (cuuint32_t)o.bn}, one[2] = {1, 1};
+    CUresult r = enc(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void *)o.w, adim, astr, abox, one,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(c, MT_ERR_CUDA, "FC tensor map A encode failed");
+    r = enc(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void *)(o.in + (uint64_t)o.in_co * es), bdim, bstr, bbox, one,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(c, MT_ERR_CUDA, "FC tensor map B encode failed");
+    CK(cudaMemcpy(ma_dev, &ma, sizeof ma, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(mb_dev, &mb, sizeof mb, cudaMemcpyHostToDevice));
+    return MT_OK;
+  }
   cuuint64_t gdim[4] = {(cuuint64_t)o.C, (cuuint64_t)o.W, (cuuint64_t)o.H, (cuuint64_t)o.N};
   cuuint64_t gstr[3] = {(cuuint64_t)o.in_cs * es, (cuuint64_t)o.W * o.in_cs * es,
                         (cuuint64_t)o.H * o.W * o.in_cs * es};

@@ -370,7 +370,7 @@ __device__ __forceinline__ ConvTile conv_tile_coords(const OpDesc &d, int tile) 
   c.n0 = nt * d.bn;
   c.kb0 = c.ks * d.kb_per_split;
   c.nk = min(d.nkb, c.kb0 + d.kb_per_split) - c.kb0;
-  if (d.tma) {
+  if (d.tma == 1 || d.tma == 2) {
     const int rg = c.mt / d.nseg, seg = c.mt - rg * d.nseg;
     c.img = rg / d.blk_tpi;
     c.ho0 = (rg - c.img * d.blk_tpi) * d.blk_rows;
@@ -384,6 +384,7 @@ __device__ __forceinline__ ConvTile conv_tile_coords(const OpDesc &d, int tile) 
 }
 // output pixel of accumulator row r (TMEM lane), or -1 if the row is padding
 __device__ __forceinline__ int conv_row_pixel(const OpDesc &d, const ConvTile &c, int r) {
+  if (d.tma == 3) return c.m0 + r < d.Co ? c.m0 + r : -1;   // tensor-core FC: row = output feature
   if (d.tma) {
     const int hl = r / d.seg_w;
     const int ho = c.ho0 + hl, wo = c.wo0 + (r - hl * d.seg_w);
@@ -415,7 +416,10 @@ __device__ void conv_tc_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaSh
       const uint32_t bar_full0 = smem_u32(&sh.bar_full[0]);
       for (int i = 0; i < d.nst && i < ct.nk; ++i) {
         mbar_expect_tx(bar_full0 + 8 * i, (uint32_t)(d.a_bytes + d.bn * 128));
-        tma_load_2d(s0 + i * d.st_bytes + d.st_boff, d.tmap_b, bar_full0 + 8 * i, (ct.kb0 + i) * MT_BK, ct.n0);
+        if (d.tma == 3)   // FC: the weights are the A (M = features) operand
+          tma_load_2d(s0 + i * d.st_bytes, d.tmap_a, bar_full0 + 8 * i, (ct.kb0 + i) * MT_BK, ct.m0);
+        else
+          tma_load_2d(s0 + i * d.st_bytes + d.st_boff, d.tmap_b, bar_full0 + 8 * i, (ct.kb0 + i) * MT_BK, ct.n0);
       }
     }
   } else {
@@ -431,6 +435,14 @@ __device__ void conv_tc_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaSh
       }
       cp_async_commit();
     }
+  }
+  if (d.tma == 3) {   // FC: per-row (feature) constants.  No L2 prefetch of the rest of the weight
+    if (tid < MT_BM) {  // stream: it is read once and would evict the other tenants' working sets
+      const int o = ct.m0 + tid;
+      sh.esc[tid] = o < d.Co ? __ldg(reinterpret_cast<const float *>(d.scale) + o) : 0.f;
+      sh.esh[tid] = o < d.Co ? __ldg(reinterpret_cast<const float *>(d.shift) + o) : 0.f;
+    }
+    return;
   }
   if (tid < d.bn) {
     const int n = ct.n0 + tid;
@@ -465,7 +477,7 @@ __device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const Conv
     const uint32_t txb = (uint32_t)(d.a_bytes + d.bn * 128);
     const uint64_t tmap_a = d.tmap_a, tmap_b = d.tmap_b;
     const int kb0 = ct.kb0, cblks = d.cblks, kw = d.kw, pw = d.pw, n0 = ct.n0, img = ct.img;
-    const int small = d.tma == 2, ntap = d.kh * d.kw;
+    const int small = d.tma == 2, ntap = d.kh * d.kw, fc = d.tma == 3, m0 = ct.m0;
     int tap = kb0 / cblks, cb = kb0 - tap * cblks;
     int rr = tap / kw, ss = tap - rr * kw;
     const int hbase = ct.ho0 * d.sh - d.ph, wbase = ct.wo0 * d.sw - pw;
@@ -476,11 +488,18 @@ __device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const Conv
       if (j > 0) mbar_wait(bar_empty0 + 8 * s, ((eph >> s) & 1u) ^ (uint32_t)((j - 1) & 1));
       if (elect_one()) {
         const uint32_t bar = bar_full0 + 8 * s;
-        if (j > 0) {
+        if (fc) {   // FC: weights (A slot) prefetched for the first nst k-blocks; input -> B slot
+          if (j > 0) {
+            mbar_expect_tx(bar, txb);
+            tma_load_2d(st, tmap_a, bar, (kb0 + i) * MT_BK, m0);
+          }
+          tma_load_2d(st + st_boff, tmap_b, bar, (kb0 + i) * MT_BK, n0);
+        } else if (j > 0) {
           mbar_expect_tx(bar, txb);
           tma_load_2d(st + st_boff, tmap_b, bar, (kb0 + i) * MT_BK, n0);
         }
-        if (small) {   // 8 taps x 8 channels: one 16-byte-row box per tap, 2 KB apart
+        if (fc) {
+        } else if (small) {   // 8 taps x 8 channels: one 16-byte-row box per tap, 2 KB apart
           int t8 = (kb0 + i) * 8;
           for (int tt = 0; tt < 8; ++tt, ++t8) {
             const int r2 = t8 / kw, s2 = t8 - r2 * kw;
@@ -630,6 +649,20 @@ __device__ __forceinline__ void conv_epilogue_vals(const RunArgs &a, const OpDes
   store_out8<bf16>(a, d, m, n, v, nvalid);
 }
 
+// tensor-core FC epilogue: accumulator row r = output feature o, 8 columns = batch images b..b+7
+__device__ __forceinline__ void fc_tc_store(const RunArgs &a, const OpDesc &d, const CtaShared &sh, int r, int o,
+                                            int b, const float *v) {
+  const float sc = sh.esc[r], sf = sh.esh[r];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    if (b + e < d.N) {
+      const float y = act_f(fmaf(v[e], sc, sf), d.act);
+      if (d.flags & OPF_OUT) a.outputs[d.tenant][(int64_t)(b + e) * d.Co + o] = y;
+      else st1(reinterpret_cast<bf16 *>(d.out) + (int64_t)(b + e) * d.out_cs + d.out_co + o, y);
+    }
+  }
+}
+
 // split-K reduce tile (tmn, rc): waits for the S partials of (M,N) tile tmn, sums columns
 // [rc*32, rc*32+32) of its valid rows in split order 0..S-1 (float4 over 4 rows), stages the sums
 // in shared memory and runs the fused epilogue.  The last of the rc reduce tiles resets the
@@ -653,11 +686,18 @@ __device__ void conv_reduce_tile(const RunArgs &a, const OpDesc &d, int rtile, u
   }
   // valid accumulator rows form a prefix of the 128 TMEM lanes
   int nv;
-  if (d.tma) nv = d.nseg > 1 ? min(d.seg_w, d.Wo - ct.wo0) : min(d.blk_rows, d.Ho - ct.ho0) * d.Wo;
+  if (d.tma == 3) nv = min(MT_BM, d.Co - ct.m0);
+  else if (d.tma) nv = d.nseg > 1 ? min(d.seg_w, d.Wo - ct.wo0) : min(d.blk_rows, d.Ho - ct.ho0) * d.Wo;
   else nv = min(MT_BM, d.M - ct.m0);
   const int c0 = rc * 32;
   const int ncol = min(32, d.bn - c0);
-  if (tid < ncol) {
+  if (d.tma == 3) {
+    if (tid < MT_BM) {
+      const int o = ct.m0 + tid;
+      sh.esc[tid] = o < d.Co ? __ldg(reinterpret_cast<const float *>(d.scale) + o) : 0.f;
+      sh.esh[tid] = o < d.Co ? __ldg(reinterpret_cast<const float *>(d.shift) + o) : 0.f;
+    }
+  } else if (tid < ncol) {
     const int n = ct.n0 + c0 + tid;
     sh.esc[c0 + tid] = n < d.Co ? __ldg(reinterpret_cast<const float *>(d.scale) + n) : 0.f;
     sh.esh[c0 + tid] = n < d.Co ? __ldg(reinterpret_cast<const float *>(d.shift) + n) : 0.f;
@@ -691,11 +731,12 @@ __device__ void conv_reduce_tile(const RunArgs &a, const OpDesc &d, int rtile, u
     const int r = it % nv, ch = it / nv;
     const int m = conv_row_pixel(d, ct, r);
     const int col = c0 + ch * 8;
-    if (m >= 0 && ct.n0 + col < d.Co) {
+    if (m >= 0 && ct.n0 + col < (d.tma == 3 ? d.N : d.Co)) {
       float v[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) v[e] = red[(ch * 8 + e) * MT_BM + r];
-      conv_epilogue_vals(a, d, sh, m, ct.n0, col, v);
+      if (d.tma == 3) fc_tc_store(a, d, sh, r, m, ct.n0 + col, v);
+      else conv_epilogue_vals(a, d, sh, m, ct.n0, col, v);
     }
   }
   __syncthreads();
@@ -780,7 +821,11 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
       for (int col = half * hcols; col < (half + 1) * hcols; col += 8) {
         float v[8];
         tmem_ld8(tl + col, v);
-        if (m >= 0 && n0 + col < d.Co) conv_epilogue_vals(a, d, sh, m, n0, col, v);
+        if (d.tma == 3) {
+          if (m >= 0 && n0 + col < d.N) fc_tc_store(a, d, sh, r, m, n0 + col, v);
+        } else if (m >= 0 && n0 + col < d.Co) {
+          conv_epilogue_vals(a, d, sh, m, n0, col, v);
+        }
       }
     }
   } else {
@@ -802,7 +847,7 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
         float v[8];
         tmem_ld8(tl + col, v);
         float *p = ws + ((int64_t)(tmn * S + ks) * d.bn + col) * MT_BM + r;
-        if (m >= 0 && n0 + col < d.Co)
+        if (m >= 0 && n0 + col < (d.tma == 3 ? d.N : d.Co))
 #pragma unroll
           for (int e = 0; e < 8; ++e) __stcg(p + e * MT_BM, v[e]);
       }
@@ -1377,6 +1422,11 @@ __device__ __forceinline__ void tile_out_range(const OpDesc &d, int tile, int64_
     case TK_CONV_TC:
       if (d.splits > 1 && tile >= d.tiles_m * d.tiles_n * d.splits)   // reduce tile -> its (M,N) tile
         tile = ((tile - d.tiles_m * d.tiles_n * d.splits) / d.rc) * d.splits;
+      if (d.tma == 3) {   // FC: batch images [n0, n0 + bn)
+        p0 = (int64_t)(((tile / d.splits) % d.tiles_n) * d.bn);
+        p1 = min((int64_t)d.N, p0 + d.bn);
+        return;
+      }
       if (d.tma) {
         const int mt = (tile / d.splits) / d.tiles_n, rg = mt / d.nseg, seg = mt - rg * d.nseg;
         const int img = rg / d.blk_tpi, ho0 = (rg - img * d.blk_tpi) * d.blk_rows;
@@ -1400,7 +1450,7 @@ __device__ __forceinline__ void tile_in_range(const OpDesc &d, int64_t p0, int64
   const int64_t HW = (int64_t)d.H * d.W;
   if (d.tk == TK_ELT) { i0 = p0; i1 = p1; return; }
   if (d.tk == TK_GAP) { i0 = p0 * HW; i1 = p1 * HW; return; }
-  if (d.tk == TK_FC) { i0 = p0 * HW; i1 = p1 * HW; return; }
+  if (d.tk == TK_FC || (d.tk == TK_CONV_TC && d.tma == 3)) { i0 = p0 * HW; i1 = p1 * HW; return; }
   const int HoWo = d.Ho * d.Wo;
   const int na = (int)(p0 / HoWo), nb = (int)((p1 - 1) / HoWo);
   const int hoa = (int)((p0 - (int64_t)na * HoWo) / d.Wo), hob = (int)((p1 - 1 - (int64_t)nb * HoWo) / d.Wo);
@@ -1413,6 +1463,11 @@ __device__ __forceinline__ void tile_in_range(const OpDesc &d, int64_t p0, int64
 __device__ __forceinline__ int tile_block(const OpDesc &d, int tile, const CtaShared &sh) {
   switch (d.tk) {
     case TK_CONV_TC: {   // block = M tile (TMA: row group, i.e. all column segments of it)
+      if (d.tma == 3) {    // FC: block = batch tile
+        const int nct = d.tiles_m * d.tiles_n * d.splits;
+        if (d.splits == 1) return tile % d.tiles_n;
+        return tile >= nct ? ((tile - nct) / d.rc) % d.tiles_n : -1;
+      }
       const int ns = d.tma ? d.nseg : 1;
       if (d.splits == 1) return tile / d.tiles_n / ns;
       const int nct = d.tiles_m * d.tiles_n * d.splits;
