@@ -183,6 +183,7 @@ static mt_status load_tenant(mt_ctx *c, int t, std::vector<std::vector<int>> &gr
 
 static mt_status plan_graphs(mt_ctx *c) {
   const int NT = (int)c->T.size();
+  const int sm_avail = std::max(24, 148 / std::max(NT, 1));   // cost model: SMs per op (shape + mix only)
   int total = 0;
   for (auto &tn : c->T) { tn.op_base = total; total += tn.L; }
   c->sum_L = total;
@@ -425,7 +426,7 @@ static mt_status plan_graphs(mt_ctx *c) {
             // A box + B box per k-block at ~160 B/ns per SM (TMA) or pays the MMA time, whichever is
             // larger; ~2.6 us of fixed cost per tile (dependency -> first data, epilogue); a split
             // adds a dependent reduce hop (~4 us fixed + the partials at ~50 B/ns per reduce tile);
-            // ~74 SMs available to the op (two tenants sharing the GPU).
+            // SMs available to the op: the GPU shared evenly by the mix's tenants (>= 37).
             int best_bn = d.bn, splits = 1;
             {
               double best = 1e30;
@@ -438,11 +439,11 @@ static mt_status plan_graphs(mt_ctx *c) {
                 for (int sp = 1; sp <= 12; ++sp) {
                   if (sp > 1 && d.nkb / sp < 2) break;
                   const int64_t kbps = cdiv(d.nkb, sp);
-                  const int64_t waves = cdiv(tmn_c * sp, 74);
+                  const int64_t waves = cdiv(tmn_c * sp, sm_avail);
                   double t = waves * (1.3 + kbps * t_kb + (sp == 1 ? 1.3 + 0.01 * bn : 0.6));
                   if (sp > 1) {
                     const int rcn = std::max(1, bn / 32);
-                    t += 4.0 + cdiv(tmn_c * rcn, 74) * (sp * rows * 32 * 4 / 50000.0);
+                    t += 4.0 + cdiv(tmn_c * rcn, sm_avail) * (sp * rows * 32 * 4 / 50000.0);
                   }
                   if (t < best * 0.97) { best = t; best_bn = bn; splits = sp; }
                 }

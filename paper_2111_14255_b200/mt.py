@@ -14,7 +14,7 @@ import re
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmt.so")
+LIB_PATH = os.environ.get("MT_LIB_PATH") or os.path.join(HERE, "libmt.so")   # override: A/B builds (tools/ab.py)
 HEADER = os.path.join(HERE, "..", "include", "mt.h")
 
 if not os.path.exists(LIB_PATH):
