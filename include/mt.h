@@ -149,6 +149,20 @@ mt_status mt_op_count(mt_ctx *ctx, int32_t tenant, int32_t *n_ops);
 mt_status mt_op_cost(mt_ctx *ctx, int32_t tenant, int32_t op, int64_t *flops, int64_t *bytes);
 /* number of work tiles an op is split into (shape-only, identical for every schedule) */
 mt_status mt_op_tiles(mt_ctx *ctx, int32_t tenant, int32_t op, int32_t *tiles);
+/* How an op is executed (introspection for tests and tuning; shape + mix only, identical for
+ * every schedule).  plan[MT_PLAN_LEN] receives: [0] kernel kind (MT_PLAN_KIND_*), [1] operand
+ * path of a tensor-core op (0 cp.async im2col, 1 TMA im2col, 2 TMA 8-channel stem, 3 TMA FC),
+ * [2] N tile (bn), [3] split-K factor, [4] M tiles, [5] N tiles, [6] pipeline stages,
+ * [7] total tiles (compute + split-K reduce), [8] column segments per output row. */
+#define MT_PLAN_LEN 9
+#define MT_PLAN_KIND_CONV_TC 0
+#define MT_PLAN_KIND_CONV_SIMT 1
+#define MT_PLAN_KIND_DW 2
+#define MT_PLAN_KIND_POOL 3
+#define MT_PLAN_KIND_GAP 4
+#define MT_PLAN_KIND_FC 5
+#define MT_PLAN_KIND_ELT 6
+mt_status mt_op_plan(mt_ctx *ctx, int32_t tenant, int32_t op, int32_t *plan);
 
 /* Device workspace: packed weights, activations, split-K partials, counters, plans. */
 mt_status mt_workspace_size(mt_ctx *ctx, size_t *bytes);

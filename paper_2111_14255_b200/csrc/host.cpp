@@ -974,6 +974,29 @@ mt_status mt_op_tiles(mt_ctx *c, int32_t t, int32_t op, int32_t *tiles) {
   return MT_OK;
 }
 
+mt_status mt_op_plan(mt_ctx *c, int32_t t, int32_t op, int32_t *plan) {
+  if (!c || !plan) return MT_ERR_ARG;
+  if (!c->loaded) return fail(c, MT_ERR_STATE, "no graphs loaded");
+  if (t < 0 || t >= (int)c->T.size() || op < 0 || op >= c->T[t].L) return fail(c, MT_ERR_ARG, "bad op");
+  const OpDesc &d = c->ops[c->T[t].op_base + op].d;
+  int kind = MT_PLAN_KIND_ELT;
+  switch (d.tk) {
+    case TK_CONV_TC: kind = MT_PLAN_KIND_CONV_TC; break;
+    case TK_CONV_SIMT: kind = MT_PLAN_KIND_CONV_SIMT; break;
+    case TK_DW: kind = MT_PLAN_KIND_DW; break;
+    case TK_POOL: kind = MT_PLAN_KIND_POOL; break;
+    case TK_GAP: kind = MT_PLAN_KIND_GAP; break;
+    case TK_FC: kind = MT_PLAN_KIND_FC; break;
+    default: break;
+  }
+  const bool tc = d.tk == TK_CONV_TC;
+  const int32_t v[MT_PLAN_LEN] = {kind, tc ? d.tma : 0, tc ? d.bn : 0, tc ? d.splits : 1, tc ? d.tiles_m : 0,
+                                  tc ? d.tiles_n : 0, tc ? (d.tma ? d.nst : MT_STAGES) : 0, d.tiles,
+                                  tc && d.tma ? d.nseg : 1};
+  for (int i = 0; i < MT_PLAN_LEN; ++i) plan[i] = v[i];
+  return MT_OK;
+}
+
 mt_status mt_workspace_size(mt_ctx *c, size_t *bytes) {
   if (!c || !bytes) return MT_ERR_ARG;
   if (!c->loaded) return fail(c, MT_ERR_STATE, "no graphs loaded");

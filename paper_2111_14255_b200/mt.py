@@ -58,6 +58,7 @@ _sig = {
     "mt_op_count": (C.c_int, [P, C.c_int32, I32P]),
     "mt_op_cost": (C.c_int, [P, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "mt_op_tiles": (C.c_int, [P, C.c_int32, C.c_int32, I32P]),
+    "mt_op_plan": (C.c_int, [P, C.c_int32, C.c_int32, I32P]),
     "mt_workspace_size": (C.c_int, [P, C.POINTER(C.c_size_t)]),
     "mt_bind_workspace": (C.c_int, [P, P, C.c_size_t]),
     "mt_set_schedule": (C.c_int, [P, C.c_int32, I32P]),
@@ -181,6 +182,16 @@ class Context:
         v = C.c_int32()
         self.check(mt_op_tiles(self.h, t, j, C.byref(v)))
         return v.value
+
+    PLAN_KEYS = ("kind", "path", "bn", "splits", "tiles_m", "tiles_n", "stages", "tiles", "segments")
+    PLAN_KINDS = ("conv_tc", "conv_simt", "dw", "pool", "gap", "fc", "elt")
+
+    def op_plan(self, t, j):
+        v = (C.c_int32 * len(self.PLAN_KEYS))()
+        self.check(mt_op_plan(self.h, t, j, v))
+        d = dict(zip(self.PLAN_KEYS, list(v)))
+        d["kind"] = self.PLAN_KINDS[d["kind"]]
+        return d
 
     def workspace_size(self):
         v = C.c_size_t()

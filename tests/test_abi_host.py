@@ -192,3 +192,29 @@ def test_host_only_context_refuses_to_run():
     with pytest.raises(mt.MTError) as e:
         c.run([0], [0])
     assert e.value.status == mt.MT_ERR_STATE
+
+
+def test_op_plans_follow_the_operand_rules():
+    """mt_op_plan: which path each op takes -- shape + mix only, so the same
+    graph gets the same plan whatever the schedule; tiles match mt_op_tiles"""
+    c = host_ctx(configs.tenants("c3"))
+    vgg = configs.tenants("c3")[1]
+    plans = [c.op_plan(1, j) for j in range(vgg.n_ops)]
+    assert all(p["tiles"] == c.op_tiles(1, j) for j, p in enumerate(plans))
+    assert plans[0]["kind"] == "conv_tc" and plans[0]["path"] == 2 and plans[0]["segments"] == 2   # 8-ch stem, 224 wide
+    assert plans[1]["path"] == 1 and plans[1]["segments"] == 2                                    # 224-wide conv: 2 x 112
+    assert plans[3]["path"] == 1 and plans[3]["segments"] == 1                                    # 112 wide: whole rows
+    fc1 = plans[18]                      # 25088 -> 4096 (205 MB of weights): tensor-core FC, split-K
+    assert fc1["kind"] == "conv_tc" and fc1["path"] == 3 and fc1["bn"] == 16 and fc1["tiles_m"] == 32
+    assert fc1["splits"] > 1 and fc1["tiles_m"] * fc1["splits"] <= 148
+    assert plans[20]["kind"] == "fc"     # 4096 -> 1000 (8.2 MB < 8 MiB): CUDA-core GEMV
+    mb = configs.tenants("c3")[2]
+    kinds = {c.op_plan(2, j)["kind"] for j in range(mb.n_ops)}
+    assert kinds == {"conv_tc", "dw", "gap", "fc"}
+    # batch 8: every FC on the tensor-core path
+    c8 = host_ctx(configs.tenants("c4b8"))
+    for t, g in enumerate(configs.tenants("c4b8")):
+        for j, nd in enumerate(g.nodes):
+            if nd["kind"] == 7:   # FC
+                p = c8.op_plan(t, j)
+                assert p["kind"] == "conv_tc" and p["path"] == 3, (g.name, j, p)
