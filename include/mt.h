@@ -220,6 +220,31 @@ mt_status mt_profile_batch_pointers(mt_ctx *ctx, int32_t n_cand, const int32_t *
                                     float *const *outputs, int32_t warmup, int32_t iters,
                                     float *lat_us, int32_t *status, void *stream);
 
+/* Analytic schedule-cost estimate: a cheap PRE-FILTER for candidate schedules,
+ * never the cost itself -- the paper rejects modeling-based costs as inaccurate and profiles
+ * (P:433-441); candidates that survive the filter are profiled with mt_profile_batch*.  Model
+ * (the contention form of SPEC.md cost_model S:229-239 plus a fixed per-op dependent-hop latency,
+ * DESIGN.md reading R19): per op j, roof_j = max(F_j/peak_flops, B_j/mem_bw) with F, B from
+ * mt_op_cost; an op is compute-bound iff F_j/peak_flops >= B_j/mem_bw.  Per stage:
+ *   chain_i = sum over tenant i's slice of (roof_j + op_latency_us)
+ *   compute = (sum F of compute-bound ops / peak_flops) * (1 + c_compute * max(0, n_c - 1) / max_concurrency)
+ *   memory  = (sum B of memory-bound ops / mem_bw)     * (1 + c_memory  * max(0, n_m - 1) / max_concurrency)
+ *   stage   = max(compute, memory, max_i chain_i) + sync_us
+ * (n_c / n_m = tenants whose slice holds a compute- / memory-bound op); est = sum of stages, us.
+ * Host-only: works on a host-only context (no GPU).  Pointer form as mt_profile_batch_pointers;
+ * status[c] = MT_OK or MT_ERR_VALIDATION (est_us[c] = NaN). */
+typedef struct mt_cost_params {
+  double peak_flops;       /* FLOP/s */
+  double mem_bw;           /* bytes/s */
+  double op_latency_us;    /* fixed latency of one dependent op hop */
+  double sync_us;          /* per-stage barrier */
+  double c_compute, c_memory;
+  int32_t max_concurrency; /* >= 1 */
+} mt_cost_params;
+mt_status mt_estimate_batch_pointers(mt_ctx *ctx, const mt_cost_params *params, int32_t n_cand,
+                                     const int32_t *cand_P, const int32_t *cand_rho, double *est_us,
+                                     int32_t *status);
+
 /* Debug: copy op `op` of tenant `tenant`'s activation (NHWC, storage precision, channels
  * [0, out_c) of its row) from the last run to host.  bytes must equal
  * batch*out_h*out_w*out_c*elem.  The graph's final op has no activation buffer. */

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <limits>
 #include <vector>
 
 #include "kernels.h"
@@ -1415,6 +1416,38 @@ mt_status mt_profile_batch_pointers(mt_ctx *c, int32_t n, const int32_t *cand_P,
     valid[k] = 1;
   }
   return profile_impl(c, n, cands, valid, inputs, outputs, warmup, iters, lat_us, status, (cudaStream_t)stream);
+}
+
+mt_status mt_estimate_batch_pointers(mt_ctx *c, const mt_cost_params *p, int32_t n, const int32_t *cand_P,
+                                     const int32_t *cand_rho, double *est_us, int32_t *status) {
+  if (!c || !p) return MT_ERR_ARG;
+  if (!c->loaded) return fail(c, MT_ERR_STATE, "no graphs loaded");
+  if (n < 0 || (n > 0 && (!cand_P || !cand_rho || !est_us || !status)) || !(p->peak_flops > 0) ||
+      !(p->mem_bw > 0) || p->max_concurrency < 1)
+    return fail(c, MT_ERR_ARG, "bad estimate arguments");
+  std::vector<int> L = lengths(c);
+  const int N = (int)L.size();
+  std::vector<std::vector<double>> F(N), B(N);
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < L[i]; ++j) {
+      const HostOp &h = c->ops[c->T[i].op_base + j];
+      F[i].push_back((double)h.flops);
+      B[i].push_back((double)h.bytes);
+    }
+  size_t off = 0;
+  std::vector<int32_t> ranges;
+  for (int k = 0; k < n; ++k) {
+    const int P = cand_P[k];
+    est_us[k] = std::numeric_limits<double>::quiet_NaN();
+    status[k] = MT_ERR_VALIDATION;
+    if (P < 0) continue;
+    const int32_t *rho = cand_rho + off;
+    off += (size_t)N * P;
+    if (pointers_to_ranges(L, P, rho, ranges).code != MT_E_OK) continue;
+    est_us[k] = estimate_schedule(F, B, P + 1, ranges.data(), *p);
+    status[k] = MT_OK;
+  }
+  return MT_OK;
 }
 
 mt_status mt_get_activation(mt_ctx *c, int32_t t, int32_t op, void *host, size_t bytes) {

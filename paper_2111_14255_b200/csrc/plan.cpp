@@ -6,6 +6,8 @@
 // two implementations share no code.
 #include "plan.h"
 
+#include <algorithm>
+
 namespace mt {
 
 static mt_error_info E(int code, int s, int t, int op) { return mt_error_info{code, s, t, op}; }
@@ -92,6 +94,38 @@ std::vector<int> sm_partition(const std::vector<bool> &active, const std::vector
     }
   for (int k = 0; k < left && k < (int)order.size(); ++k) out[order[k]] += 1;
   return out;
+}
+
+// Pre-filter estimate (include/mt.h mt_estimate_batch_pointers; reading R19).
+double estimate_schedule(const std::vector<std::vector<double>> &flops,
+                         const std::vector<std::vector<double>> &bytes, int S, const int32_t *ranges,
+                         const mt_cost_params &p) {
+  const int N = (int)flops.size();
+  const double us = 1e6;
+  double total = 0.0;
+  for (int k = 0; k < S; ++k) {
+    double C = 0.0, M = 0.0, chain_max = 0.0;
+    int n_c = 0, n_m = 0;
+    for (int i = 0; i < N; ++i) {
+      const int a = ranges[(k * N + i) * 2], b = ranges[(k * N + i) * 2 + 1];
+      double chain = 0.0;
+      bool has_c = false, has_m = false;
+      for (int j = a; j < b; ++j) {
+        const double tc = flops[i][j] / p.peak_flops * us, tm = bytes[i][j] / p.mem_bw * us;
+        chain += std::max(tc, tm) + p.op_latency_us;
+        if (tc >= tm) { C += flops[i][j]; has_c = true; }
+        else { M += bytes[i][j]; has_m = true; }
+      }
+      n_c += has_c;
+      n_m += has_m;
+      chain_max = std::max(chain_max, chain);
+    }
+    const double mc = (double)std::max(1, p.max_concurrency);
+    const double compute = C / p.peak_flops * us * (1.0 + p.c_compute * std::max(0, n_c - 1) / mc);
+    const double memory = M / p.mem_bw * us * (1.0 + p.c_memory * std::max(0, n_m - 1) / mc);
+    total += std::max(std::max(compute, memory), chain_max) + p.sync_us;
+  }
+  return total;
 }
 
 }  // namespace mt

@@ -76,5 +76,9 @@ mt_error_info pointers_to_ranges(const std::vector<int> &L, int P, const int32_t
                                  std::vector<int32_t> &ranges);
 std::vector<int> sm_partition(const std::vector<bool> &active,
                               const std::vector<__int128> &w, int n_sms);
+// analytic pre-filter cost of one valid schedule (ranges [S][N][2]); flops/bytes per tenant op
+double estimate_schedule(const std::vector<std::vector<double>> &flops,
+                         const std::vector<std::vector<double>> &bytes, int S, const int32_t *ranges,
+                         const mt_cost_params &p);
 
 }  // namespace mt

@@ -43,6 +43,12 @@ class mt_graph(C.Structure):
                 ("in_c", C.c_int32), ("in_h", C.c_int32), ("in_w", C.c_int32), ("precision", C.c_int32)]
 
 
+class mt_cost_params(C.Structure):
+    _fields_ = [("peak_flops", C.c_double), ("mem_bw", C.c_double), ("op_latency_us", C.c_double),
+                ("sync_us", C.c_double), ("c_compute", C.c_double), ("c_memory", C.c_double),
+                ("max_concurrency", C.c_int32)]
+
+
 class mt_error_info(C.Structure):
     _fields_ = [("code", C.c_int32), ("stage", C.c_int32), ("tenant", C.c_int32), ("op", C.c_int32)]
 
@@ -59,6 +65,8 @@ _sig = {
     "mt_op_cost": (C.c_int, [P, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "mt_op_tiles": (C.c_int, [P, C.c_int32, C.c_int32, I32P]),
     "mt_op_plan": (C.c_int, [P, C.c_int32, C.c_int32, I32P]),
+    "mt_estimate_batch_pointers": (C.c_int, [P, C.POINTER(mt_cost_params), C.c_int32, I32P, I32P,
+                                             C.POINTER(C.c_double), I32P]),
     "mt_workspace_size": (C.c_int, [P, C.POINTER(C.c_size_t)]),
     "mt_bind_workspace": (C.c_int, [P, P, C.c_size_t]),
     "mt_set_schedule": (C.c_int, [P, C.c_int32, I32P]),
@@ -274,6 +282,20 @@ class Context:
                                              _ptrs(in_ptrs), _ptrs(out_ptrs), warmup, iters,
                                              lat.ctypes.data_as(F32P), st.ctypes.data_as(I32P), P(stream)))
         return lat, st
+
+    def estimate_batch_pointers(self, cands, peak_flops, mem_bw, op_latency_us, sync_us, c_compute=0.0,
+                                c_memory=0.0, max_concurrency=1):
+        """analytic pre-filter estimate (us) per candidate (include/mt.h); host-only"""
+        n = len(cands)
+        Ps = np.array([len(r[0]) if len(r) else 0 for r in cands], np.int32)
+        flat = np.concatenate([np.asarray(r, np.int32).reshape(-1) for r in cands] + [np.zeros(1, np.int32)])
+        est = np.zeros(n, np.float64)
+        st = np.zeros(n, np.int32)
+        prm = mt_cost_params(peak_flops, mem_bw, op_latency_us, sync_us, c_compute, c_memory, max_concurrency)
+        self.check(mt_estimate_batch_pointers(self.h, C.byref(prm), n, Ps.ctypes.data_as(I32P),
+                                              flat.ctypes.data_as(I32P),
+                                              est.ctypes.data_as(C.POINTER(C.c_double)), st.ctypes.data_as(I32P)))
+        return est, st
 
     def profile_batch(self, cand_ranges, in_ptrs, out_ptrs, warmup=2, iters=10, stream=0):
         n = len(cand_ranges)

@@ -89,3 +89,19 @@ def coordinate_descent(profile_fn, lengths, P: int, rounds: int, m: int, seed: i
                 kbest = min(ok, key=lambda k: (lat[k], k))
                 rho = cands[kbest]
     return res                                    # L14-15: global best of D
+
+
+def prefiltered_search(estimate_fn, profile_fn, candidates, keep: int) -> SearchResult:
+    """rank `candidates` by the analytic estimate (estimate_fn(cands) -> (est,
+    status), e.g. Context.estimate_batch_pointers; microseconds of host time per candidate), then
+    profile only the `keep` best-estimated feasible ones -- the cost stays the profiled latency
+    (P:441).  Returns the SearchResult of the profiled subset; `records` holds only those."""
+    est, est_st = estimate_fn(candidates)
+    ok = [k for k in range(len(candidates)) if est_st[k] == 0 and np.isfinite(est[k])]
+    ok.sort(key=lambda k: (est[k], k))
+    chosen = [candidates[k] for k in ok[:keep]]
+    res = SearchResult(best_rho=None, best_lat=float("inf"))
+    if chosen:
+        lat, st = profile_fn(chosen)
+        _record(res, chosen, lat, st)
+    return res
