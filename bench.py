@@ -220,7 +220,7 @@ def main():
         results[name] = float(np.mean(t))
     head_name = min(results, key=results.get)
     ctx.set_schedule_pointers(named[head_name])
-    S = ctx.num_stages()
+    n_stages = ctx.num_stages()
 
     # ---- headline timed region (clocks sampled throughout) ----
     with ClockSampler(local) as clk:
@@ -294,9 +294,9 @@ def main():
         # Alg.1 coordinate descent on the same mix (P=3, R=1, M=8), rank 0's GPU
         search_line = None
         if rank == 0:
-            from paper_2111_14255_b200 import search as S
+            from paper_2111_14255_b200 import search as search_mod
             t1 = time.perf_counter()
-            cdr = S.coordinate_descent(pfn, PL, P=3, rounds=1, m=8, seed=14255)
+            cdr = search_mod.coordinate_descent(pfn, PL, P=3, rounds=1, m=8, seed=14255)
             search_line = {"algorithm": "coordinate descent (Alg.1), P=3 R=1 M=8", "evaluations": cdr.evaluations,
                            "best_us": cdr.best_lat, "start_us": cdr.records[0][1],
                            "wall_s": time.perf_counter() - t1}
@@ -324,7 +324,7 @@ def main():
             "dtype": "bf16", "data": "synthetic (seeded LeCun-normal weights, identity-BN, N(0,1) input)",
             "config": {"workload": f"{args.config} ({CONFIG_NAMES.get(args.config, args.config)}): "
                                    + configs.CONFIGS[args.config][3],
-                       "schedule": head_name, "stages": S,
+                       "schedule": head_name, "stages": n_stages,
                        "l2": "warm" if args.warm_l2 else "flushed before every timed step (256 MiB write)",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
             "gpu_launches": K,
