@@ -513,6 +513,7 @@ static mt_status plan_graphs(mt_ctx *c) {
             d.tk = TK_CONV_TC;
             d.kh = d.kw = 1;
             d.cblks = 1;
+            d.nseg = 1;
             d.M = os.c;
             d.bn = g.batch <= 16 ? 16 : 32;
             d.tiles_n = (int)cdiv(g.batch, d.bn);

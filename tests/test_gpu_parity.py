@@ -209,3 +209,32 @@ def test_search_drivers_on_gpu_profiler():
     assert rs.best_rho is not None and np.isfinite(rs.best_lat)
     m.ctx.set_schedule_pointers(cd.best_rho)
     m.run()
+
+
+def test_operand_path_edge_cases():
+    """ragged tensor-core paths: 147-wide rows (column segments 74 + 73) on the 8-channel stem and
+    the 64-channel TMA path, strided segments, a tensor-core FC at batch 3 with K % 64 != 0,
+    Co % 128 != 0 and a flattened 3x3 spatial input, and the CUDA-core FC after it"""
+    from paper_2111_14255_b200.session import TenantMix
+    b = zoo.GraphBuilder("tinyA", 3, 3, 147, 147, zoo.PREC_BF16, seed=5)
+    x0 = b.conv(-1, 64, 3, 1, 1)                  # stem, 147 wide -> 2 segments
+    x1 = b.conv(x0, 64, 3, 1, 1)                  # TMA mode 1, 2 segments, ragged last
+    x2 = b.conv(x1, 104, 3, 2, 1)                 # 74 wide, stride 2
+    x3 = b.maxpool(x2, 3, 2, 0)                   # 36
+    x4 = b.maxpool(x3, 5, 5, 0)                   # 7 x 7 x 104 -> K = 5096 (79.6 k-blocks)
+    x5 = b.fc(x4, 200, act=zoo.ACT_RELU)          # b=3 -> tensor-core FC, Co = 200, split-K
+    b.fc(x5, 10)
+    g = b.build()
+    m = TenantMix([g])
+    plans = [m.ctx.op_plan(0, j) for j in range(g.n_ops)]
+    assert plans[0]["segments"] == 2 and plans[0]["path"] == 2
+    assert plans[1]["segments"] == 2 and plans[1]["path"] == 1
+    assert plans[5]["path"] == 3 and plans[5]["splits"] > 1     # batch 3: both FCs on tensor cores
+    assert plans[6]["path"] == 3
+    x = zoo.make_input(g, seed=6)
+    m.set_input(x)
+    m.ctx.set_schedule_pointers([[2, 5]])
+    m.run()
+    errs = teacher_forced_errors(m, x, 0)
+    assert max(errs) <= 1e-2, errs
+    assert rel_err(m.outputs_numpy()[0], fw.forward(g, x, "bf16")) <= 1e-2
