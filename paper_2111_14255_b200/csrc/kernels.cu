@@ -138,7 +138,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // waiting warps that are not on the tile's critical issue path back off between probes so they
 // do not take issue slots from the TMA-producer / MMA lanes
 __device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) __nanosleep(64);
+  // try_wait with a suspend-time hint: the warp is parked by the hardware until the phase
+  // completes (or the hint elapses) -- no issue slots taken, no oversleeping
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(1000000u)
+        : "memory");
+  }
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -173,6 +184,18 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float *v) {
   v[0] = __uint_as_float(r0); v[1] = __uint_as_float(r1); v[2] = __uint_as_float(r2);
   v[3] = __uint_as_float(r3); v[4] = __uint_as_float(r4); v[5] = __uint_as_float(r5);
   v[6] = __uint_as_float(r6); v[7] = __uint_as_float(r7);
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 // 32 lanes x 32 bit x 32 columns in one load (one wait for 32 accumulator columns)
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
@@ -633,20 +656,33 @@ __device__ __forceinline__ void conv_tc_mainloop_cpasync(const RunArgs &a, const
   cp_async_wait<0>();
 }
 
-__device__ __forceinline__ void conv_epilogue_vals(const RunArgs &a, const OpDesc &d, const CtaShared &sh,
-                                                   int m, int n0, int col, float *v) {
-  const int n = n0 + col;
-  const int nvalid = min(8, d.Co - n);
-  float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+// residual of output pixel m, channels n..n+7 (zeros past Co or without a residual)
+__device__ __forceinline__ void conv_residual8(const OpDesc &d, int m, int n, float *r) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) r[e] = 0.f;
   if (d.flags & OPF_RES) {
+    const int nvalid = min(8, d.Co - n);
     const bf16 *rp = reinterpret_cast<const bf16 *>(d.res) + (int64_t)m * d.res_cs + d.res_co + n;
-    if (nvalid == 8) ld8_cg(rp, r);
-    else
-      for (int e = 0; e < nvalid; ++e) r[e] = ld1_cg(rp + e);
+    if (nvalid == 8) {
+      ld8_cg(rp, r);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) r[e] = e < nvalid ? ld1_cg(rp + e) : 0.f;   // static indices
+    }
   }
+}
+__device__ __forceinline__ void conv_epilogue_store(const RunArgs &a, const OpDesc &d, const CtaShared &sh,
+                                                    int m, int n0, int col, float *v, const float *r) {
+  const int n = n0 + col;
 #pragma unroll
   for (int e = 0; e < 8; ++e) v[e] = act_f(fmaf(v[e], sh.esc[col + e], sh.esh[col + e]) + r[e], d.act);
-  store_out8<bf16>(a, d, m, n, v, nvalid);
+  store_out8<bf16>(a, d, m, n, v, min(8, d.Co - n));
+}
+__device__ __forceinline__ void conv_epilogue_vals(const RunArgs &a, const OpDesc &d, const CtaShared &sh,
+                                                   int m, int n0, int col, float *v) {
+  float r[8];
+  conv_residual8(d, m, n0 + col, r);
+  conv_epilogue_store(a, d, sh, m, n0, col, v, r);
 }
 
 // tensor-core FC epilogue: accumulator row r = output feature o, 8 columns = batch images b..b+7
@@ -784,7 +820,6 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
   if (S == 1) {
     if (hcols >= 32) {
       for (int cb = half * hcols; cb < (half + 1) * hcols; cb += 32) {
-        if (tid == 0 && cb == 0) sh.t_kb[0] = gtimer();
         // residual of these 32 columns requested before the TMEM drain (hides its L2 latency)
         uint4 rr[4] = {};
         const bool okrow = m >= 0;
@@ -795,7 +830,6 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
         }
         float v[32];
         tmem_ld32(tl + cb, v);
-        if (tid == 0 && cb == 0) sh.t_kb[1] = gtimer();
         if (okrow) {
           if ((d.flags & OPF_RES) && n0 + cb + 32 <= d.Co) {
 #pragma unroll
@@ -815,6 +849,28 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
             for (int j = 0; j < 4; ++j)
               if (n0 + cb + j * 8 < d.Co) conv_epilogue_vals(a, d, sh, m, n0, cb + j * 8, v + j * 8);
           }
+        }
+      }
+    } else if (hcols == 16 && d.tma != 3 && n0 + half * 16 + 16 <= d.Co) {
+      // bn = 32, both 8-column groups valid: the residual (packed bf16) is requested before the
+      // TMEM drain and both groups come out of one TMEM load + wait
+      const int c0 = half * 16;
+      uint4 rr[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+      if ((d.flags & OPF_RES) && m >= 0) {
+        const bf16 *rp = reinterpret_cast<const bf16 *>(d.res) + (int64_t)m * d.res_cs + d.res_co + n0 + c0;
+        rr[0] = __ldcg(reinterpret_cast<const uint4 *>(rp));
+        rr[1] = __ldcg(reinterpret_cast<const uint4 *>(rp) + 1);
+      }
+      float v[16];
+      tmem_ld16(tl + c0, v);
+      if (m >= 0) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          Raw8<bf16> raw;
+          raw.u = rr[j];
+          float rf[8];
+          cvt8(raw, rf);
+          conv_epilogue_store(a, d, sh, m, n0, c0 + 8 * j, v + 8 * j, rf);
         }
       }
     } else {
@@ -855,10 +911,8 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
     // published together with the tile's completion in run_stage (one fence for all counters)
     if (tid == 0) sh.xrel = a.splitcnt + d.cnt_off + tmn;
   }
-  if (tid == 0) sh.t_kb[2] = gtimer();
   tc_fence_before();
   __syncthreads();
-  if (tid == 0) sh.t_kb[3] = gtimer();
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1644,19 +1698,23 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
       int op = -1, tile = 0, ten = -1;
       // visiting order: home tenant first; then (steal 1) round-robin or (steal 2) the tenant with
       // the most unclaimed ops of its slice first (critical-path-first list scheduling)
-      int order[MT_MAXT];
-      order[0] = sh.home;
-      int no = 1;
-      for (int q = 1; q < T; ++q) order[no++] = (sh.home + q) % T;
-      if (a.steal == 2)
-        for (int i = 1; i < no; ++i)
-          for (int j = i + 1; j < no; ++j) {
-            const int ri = sh.end[order[i]] - sh.cur[order[i]], rj = sh.end[order[j]] - sh.cur[order[j]];
-            if (rj > ri) { const int x = order[i]; order[i] = order[j]; order[j] = x; }
-          }
+      // (selection on the fly, no local array: ties go to the earlier tenant in round-robin order)
+      unsigned visited = 0;
       for (int q = 0; q < T && op < 0; ++q) {
         if (!a.steal && q > 0) break;
-        const int t = order[q];
+        int t = sh.home + q;
+        if (t >= T) t -= T;
+        if (q > 0 && a.steal == 2) {
+          int best = -1, bestr = -1;
+          for (int k = 1; k < T; ++k) {
+            int c = sh.home + k;
+            if (c >= T) c -= T;
+            const int rem = sh.end[c] - sh.cur[c];
+            if (!((visited >> c) & 1u) && rem > bestr) { bestr = rem; best = c; }
+          }
+          t = best;
+        }
+        visited |= 1u << t;
         while (sh.cur[t] < sh.end[t]) {
           const int o = sh.cur[t];
           const int k = atomicAdd(a.claim + o, 1);
