@@ -118,7 +118,13 @@ typedef enum {
                            /* 2 (default): ... the tenant with most unclaimed ops first     */
   MT_OPT_NUM_SMS = 2,      /* host-only contexts: SM count used for the partition (148)    */
   MT_OPT_TIMEOUT_MS = 3,   /* device spin timeout (default 2000 ms)                         */
-  MT_OPT_CTAS_PER_SM = 4   /* reserved (1)                                                  */
+  MT_OPT_CTAS_PER_SM = 4,  /* reserved (1)                                                  */
+  MT_OPT_PARTITION = 5     /* SM partition rule per stage (a3; R16 / R16b):       */
+                           /* 0 (default): n_t proportional to the slice's roofline time    */
+                           /*    (north star); 1: latency-balanced -- minimise max_t E_t,   */
+                           /*    E_t(n) = sum over the slice's work items ceil(tiles/n)*ns  */
+                           /*    (mt_op_work); 2: work/span, E_t(n) = ceil(W_t/n) + S_t.    */
+                           /*    Setting it re-plans the active schedule.                   */
 } mt_option;
 
 /* execution modes of mt_run_baseline: the same tile functions launched one kernel per op */
@@ -163,6 +169,11 @@ mt_status mt_op_tiles(mt_ctx *ctx, int32_t tenant, int32_t op, int32_t *tiles);
 #define MT_PLAN_KIND_FC 5
 #define MT_PLAN_KIND_ELT 6
 mt_status mt_op_plan(mt_ctx *ctx, int32_t tenant, int32_t op, int32_t *plan);
+/* Latency model of one op (input of the MT_OPT_PARTITION = 1 rule; shape + mix only):
+ * tiles[2] = compute tiles, split-K reduce tiles (0 without split-K); ns[2] = estimated
+ * nanoseconds of one tile of each (calibrated on device traces).
+ * Host arrays of 2 elements, written on MT_OK; MT_ERR_STATE before mt_load_graphs. */
+mt_status mt_op_work(mt_ctx *ctx, int32_t tenant, int32_t op, int32_t *tiles, int64_t *ns);
 
 /* Device workspace: packed weights, activations, split-K partials, counters, plans. */
 mt_status mt_workspace_size(mt_ctx *ctx, size_t *bytes);
@@ -179,7 +190,8 @@ mt_status mt_num_stages(mt_ctx *ctx, int32_t *n_stages);
 mt_status mt_get_schedule(mt_ctx *ctx, int32_t *ranges);
 /* stage_of[concat_i L_i]: stage index of op j of tenant i */
 mt_status mt_stage_assignment(mt_ctx *ctx, int32_t *stage_of);
-/* sms[S][N]: CTAs whose home queue is tenant i in stage s (runtime-aware partition, a3) */
+/* sms[S][N]: CTAs whose home queue is tenant i in stage s (runtime-aware partition, a3;
+ * rule chosen by MT_OPT_PARTITION; every active tenant >= 1, inactive 0, sum = #SMs) */
 mt_status mt_sm_partition(mt_ctx *ctx, int32_t *sms);
 
 /* Run the active schedule once on the persistent stage executor (one cooperative launch).

@@ -231,6 +231,39 @@ def sm_partition(weights, n_sms):
     return out
 
 
+def sm_partition_balanced(items, n_sms, mode=1, hop_ns=2000):
+    """Latency-balanced SM partition (reading R16b; not in the paper -- the north
+    star's runtime-aware partition with a latency rather than a roofline weight).
+    items[t] = None (empty slice) or the list of (tiles, ns) work items of tenant t's slice.
+    With n CTAs tenant t needs E_t(n) = sum over its items of ceil(tiles / n) * ns.
+    Start: every active tenant 1 CTA.  Then, one CTA at a time, give it to the active tenant
+    with the largest E_t among those with n_t < cap_t (cap_t = largest item tile count), ties
+    to the lower index; when every active tenant is capped, to the largest E_t regardless.
+    Inactive tenants get 0.
+    mode 2 (work/span, Brent's bound) instead uses E_t(n) = ceil(W_t / n) + S_t with
+    W_t = sum tiles*ns and S_t = sum (ns + hop_ns) over the items."""
+    N = len(items)
+    out = [0] * N
+    act = [t for t in range(N) if items[t] is not None]
+    if not act:
+        return out
+
+    def E(t, n):
+        if mode == 2:
+            W = sum(k * ns for k, ns in items[t])
+            return -(-W // n) + sum(ns + hop_ns for _, ns in items[t])
+        return sum(-(-k // n) * ns for k, ns in items[t])
+
+    cap = {t: max([k for k, _ in items[t]] or [0]) for t in act}
+    for t in act:
+        out[t] = 1
+    for _ in range(n_sms - len(act)):
+        cand = [t for t in act if out[t] < cap[t]] or act
+        best = max(cand, key=lambda t: (E(t, out[t]), -t))
+        out[best] += 1
+    return out
+
+
 def stage_weights(graphs, ranges, elem_bytes_of):
     """Per-stage per-tenant weights for sm_partition (None for an empty slice)."""
     res = []

@@ -20,6 +20,7 @@ using namespace mt;
 
 static const int64_t BW_GBS = 8000;        // spec HBM GB/s (north star "8 TB/s")
 static const int64_t TC_GFLOPS = 2250000;  // spec dense bf16 GFLOP/s (2.25 PFLOP/s)
+static const int64_t MT_HOP_NS = 2000;     // partition mode 2: dependency hop between ops (traces)
 
 struct mt_ctx {
   int device = -1;
@@ -27,6 +28,7 @@ struct mt_ctx {
   int n_sms = 148;
   int grid = 148;
   int steal = 2;
+  int partition = 0;   // MT_OPT_PARTITION: 0 roofline-proportional, 1 latency-balanced, 2 work/span
   int64_t timeout_ms = 2000;
   bool loaded = false, bound = false, has_sched = false;
   std::vector<Tenant> T;
@@ -586,6 +588,35 @@ static mt_status plan_graphs(mt_ctx *c) {
     nblk_total += d.nblk;
   }
   c->total_blocks = (int)nblk_total;
+  // ---- latency model of every op (partition input, R16b): tiles x ns per tile ----
+  // Same calibration as the (bn, splits) choice above: per k-block max(MMA, A+B bytes at ~160 B/ns
+  // per SM), ~2.6 us fixed per tile; split-K reduce tiles read their partials at ~50 B/ns; the
+  // memory-bound kinds ~2.6 us fixed + their bytes per tile at ~50 B/ns.
+  for (auto &h : c->ops) {
+    const OpDesc &d = h.d;
+    double us0 = 0.0, us1 = 0.0;
+    int64_t t0 = d.tiles, t1 = 0;
+    if (d.tk == TK_CONV_TC) {
+      const double a_kb = d.tma ? (double)d.a_bytes : 16384.0;
+      const double rows = d.tma == 3 ? 128.0 : d.tma ? (double)d.blk_rows * d.seg_w : 128.0;
+      const double t_kb = std::max(0.13 * d.bn / 128.0, (a_kb + d.bn * 128.0) / 160000.0);
+      const int64_t tmn = (int64_t)d.tiles_m * d.tiles_n;
+      t0 = tmn * d.splits;
+      us0 = 1.3 + d.kb_per_split * t_kb + (d.splits == 1 ? 1.3 + 0.01 * d.bn : 0.6);
+      if (d.splits > 1) {
+        t1 = tmn * d.rc;
+        us1 = 2.6 + d.splits * rows * 32 * 4 / 50000.0;
+      }
+    } else if (d.tk == TK_CONV_SIMT) {
+      us0 = 3.0 + 2.0 * MT_SIMT_BM * MT_SIMT_BN * d.K / 50000.0;
+    } else {
+      us0 = 2.6 + (double)h.bytes / std::max(1, d.tiles) / 50000.0;
+    }
+    h.work_tiles[0] = (int32_t)t0;
+    h.work_ns[0] = (int64_t)llround(us0 * 1000.0);
+    h.work_tiles[1] = (int32_t)t1;
+    h.work_ns[1] = t1 ? (int64_t)llround(us1 * 1000.0) : 0;
+  }
   c->weight_bytes = wbytes;
   c->partial_bytes = pbytes;
   c->total_split_cnt = split_cnt;
@@ -661,7 +692,21 @@ static void build_stage_plan(mt_ctx *c, Schedule &s) {
         w[t] += a > bb ? a : bb;
       }
     }
-    std::vector<int> n = sm_partition(active, w, c->n_sms);
+    std::vector<int> n;
+    if (c->partition >= 1) {
+      std::vector<std::vector<std::pair<int64_t, int64_t>>> items(N);
+      for (int t = 0; t < N; ++t) {
+        if (!active[t]) continue;
+        for (int j = s.ranges[(k * N + t) * 2]; j < s.ranges[(k * N + t) * 2 + 1]; ++j) {
+          const HostOp &h = c->ops[c->T[t].op_base + j];
+          for (int q = 0; q < 2; ++q)
+            if (h.work_tiles[q] > 0) items[t].push_back({h.work_tiles[q], h.work_ns[q]});
+        }
+      }
+      n = sm_partition_balanced(active, items, c->n_sms, c->partition, MT_HOP_NS);
+    } else {
+      n = sm_partition(active, w, c->n_sms);
+    }
     int cta = 0;
     for (int t = 0; t < N; ++t) {
       s.sms[k * N + t] = n[t];
@@ -920,6 +965,14 @@ mt_status mt_set_option(mt_ctx *c, int32_t option, int64_t value) {
       c->timeout_ms = value;
       return MT_OK;
     case MT_OPT_CTAS_PER_SM: return value == 1 ? MT_OK : fail(c, MT_ERR_ARG, "only 1 CTA/SM");
+    case MT_OPT_PARTITION:
+      if (value < 0 || value > 2) return fail(c, MT_ERR_ARG, "partition must be 0, 1 or 2");
+      c->partition = (int)value;
+      if (c->has_sched) {
+        Schedule s = c->sched;
+        return apply_schedule(c, s);
+      }
+      return MT_OK;
   }
   return fail(c, MT_ERR_ARG, "unknown option");
 }
@@ -996,6 +1049,18 @@ mt_status mt_op_plan(mt_ctx *c, int32_t t, int32_t op, int32_t *plan) {
                                   tc ? d.tiles_n : 0, tc ? (d.tma ? d.nst : MT_STAGES) : 0, d.tiles,
                                   tc && d.tma ? d.nseg : 1};
   for (int i = 0; i < MT_PLAN_LEN; ++i) plan[i] = v[i];
+  return MT_OK;
+}
+
+mt_status mt_op_work(mt_ctx *c, int32_t t, int32_t op, int32_t *tiles, int64_t *ns) {
+  if (!c || !tiles || !ns) return MT_ERR_ARG;
+  if (!c->loaded) return fail(c, MT_ERR_STATE, "no graphs loaded");
+  if (t < 0 || t >= (int)c->T.size() || op < 0 || op >= c->T[t].L) return fail(c, MT_ERR_ARG, "bad op");
+  const HostOp &h = c->ops[c->T[t].op_base + op];
+  for (int q = 0; q < 2; ++q) {
+    tiles[q] = h.work_tiles[q];
+    ns[q] = h.work_ns[q];
+  }
   return MT_OK;
 }
 

@@ -96,6 +96,59 @@ std::vector<int> sm_partition(const std::vector<bool> &active, const std::vector
   return out;
 }
 
+// Latency-balanced partition (reading R16b).  Tenant t's slice is a list of work items
+// (tiles, ns per tile); with n CTAs its estimated time is E_t(n) = sum ceil(tiles / n) * ns
+// (a tenant's ops run one after another, each in ceil(tiles / n) waves).  Every active tenant
+// starts with one CTA; each remaining CTA goes to the tenant with the largest E_t among those
+// with n_t < cap_t (cap = most tiles of one item; more CTAs than that cannot shorten the slice),
+// ties to the lower index; once every tenant is capped, to the largest E_t regardless.  Greedy
+// "feed the current maximum" minimises max_t E_t exactly (each E_t is non-increasing in n).
+// mode 2 (work/span, Brent): E_t(n) = ceil(W_t / n) + S_t with W_t = sum tiles * ns (busy time)
+// and S_t = sum (ns + hop_ns) (the chain's latency floor: consecutive ops overlap as a wavefront,
+// so a tenant is either throughput-bound on its n CTAs or latency-bound on its chain).
+static int64_t est_time(const std::vector<std::pair<int64_t, int64_t>> &items, int n, int mode,
+                        int64_t hop_ns) {
+  int64_t e = 0;
+  if (mode == 2) {
+    int64_t w = 0;
+    for (const auto &it : items) {
+      w += it.first * it.second;
+      e += it.second + hop_ns;
+    }
+    return e + (w + n - 1) / n;
+  }
+  for (const auto &it : items) e += (it.first + n - 1) / n * it.second;
+  return e;
+}
+
+std::vector<int> sm_partition_balanced(const std::vector<bool> &active,
+                                       const std::vector<std::vector<std::pair<int64_t, int64_t>>> &items,
+                                       int n_sms, int mode, int64_t hop_ns) {
+  const int N = (int)active.size();
+  std::vector<int> out(N, 0);
+  std::vector<int64_t> E(N, 0), cap(N, 0);
+  int A = 0;
+  for (int t = 0; t < N; ++t) {
+    if (!active[t]) continue;
+    ++A;
+    out[t] = 1;
+    for (const auto &it : items[t]) cap[t] = std::max(cap[t], it.first);
+    E[t] = est_time(items[t], 1, mode, hop_ns);
+  }
+  if (A == 0) return out;
+  for (int left = n_sms - A; left > 0; --left) {
+    int best = -1;
+    for (int pass = 0; pass < 2 && best < 0; ++pass)
+      for (int t = 0; t < N; ++t) {
+        if (!active[t] || (pass == 0 && out[t] >= cap[t])) continue;
+        if (best < 0 || E[t] > E[best]) best = t;
+      }
+    out[best] += 1;
+    E[best] = est_time(items[best], out[best], mode, hop_ns);
+  }
+  return out;
+}
+
 // Pre-filter estimate (include/mt.h mt_estimate_batch_pointers; reading R19).
 double estimate_schedule(const std::vector<std::vector<double>> &flops,
                          const std::vector<std::vector<double>> &bytes, int S, const int32_t *ranges,

@@ -3,6 +3,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/mt.h"
@@ -38,6 +39,8 @@ struct WPack {        // one weight repack job executed at bind
 struct HostOp {
   OpDesc d{};
   int64_t flops = 0, bytes = 0;     // algorithmic cost (SURVEY d.4)
+  int32_t work_tiles[2] = {0, 0};   // latency model (R16b): compute tiles, reduce tiles
+  int64_t work_ns[2] = {0, 0};      // ... and the estimated ns of one tile of each
   TensorView out, res;
   TensorView in[MT_MAXIN];
   int n_in = 0;
@@ -76,6 +79,10 @@ mt_error_info pointers_to_ranges(const std::vector<int> &L, int P, const int32_t
                                  std::vector<int32_t> &ranges);
 std::vector<int> sm_partition(const std::vector<bool> &active,
                               const std::vector<__int128> &w, int n_sms);
+// latency-balanced partition: items[t] = (tiles, ns per tile) of each op of tenant t's slice
+std::vector<int> sm_partition_balanced(const std::vector<bool> &active,
+                                       const std::vector<std::vector<std::pair<int64_t, int64_t>>> &items,
+                                       int n_sms, int mode, int64_t hop_ns);
 // analytic pre-filter cost of one valid schedule (ranges [S][N][2]); flops/bytes per tenant op
 double estimate_schedule(const std::vector<std::vector<double>> &flops,
                          const std::vector<std::vector<double>> &bytes, int S, const int32_t *ranges,

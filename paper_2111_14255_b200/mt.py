@@ -24,7 +24,7 @@ lib = C.CDLL(LIB_PATH)
 MT_OK, MT_ERR_INTERNAL, MT_ERR_VALIDATION, MT_ERR_REFUSED, MT_ERR_CUDA, MT_ERR_ARG, MT_ERR_STATE = range(7)
 MT_MAX_INPUTS = 8
 MT_MAX_TENANTS = 16
-MT_OPT_STEAL, MT_OPT_NUM_SMS, MT_OPT_TIMEOUT_MS = 1, 2, 3
+MT_OPT_STEAL, MT_OPT_NUM_SMS, MT_OPT_TIMEOUT_MS, MT_OPT_PARTITION = 1, 2, 3, 5
 BASE_MODES = {"seq": 1, "ms_dfs": 2, "ms_bfs": 3, "seq_graph": 4, "ms_graph": 5, "stage_events": 6}
 
 
@@ -65,6 +65,7 @@ _sig = {
     "mt_op_cost": (C.c_int, [P, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "mt_op_tiles": (C.c_int, [P, C.c_int32, C.c_int32, I32P]),
     "mt_op_plan": (C.c_int, [P, C.c_int32, C.c_int32, I32P]),
+    "mt_op_work": (C.c_int, [P, C.c_int32, C.c_int32, I32P, C.POINTER(C.c_int64)]),
     "mt_estimate_batch_pointers": (C.c_int, [P, C.POINTER(mt_cost_params), C.c_int32, I32P, I32P,
                                              C.POINTER(C.c_double), I32P]),
     "mt_workspace_size": (C.c_int, [P, C.POINTER(C.c_size_t)]),
@@ -200,6 +201,13 @@ class Context:
         d = dict(zip(self.PLAN_KEYS, list(v)))
         d["kind"] = self.PLAN_KINDS[d["kind"]]
         return d
+
+    def op_work(self, t, j):
+        """[(tiles, ns per tile)] work items of op j (mt_op_work; split-K reduce tiles second)."""
+        tiles = (C.c_int32 * 2)()
+        ns = (C.c_int64 * 2)()
+        self.check(mt_op_work(self.h, t, j, tiles, ns))
+        return [(int(tiles[q]), int(ns[q])) for q in range(2) if tiles[q] > 0]
 
     def workspace_size(self):
         v = C.c_size_t()

@@ -53,6 +53,25 @@ class TenantMix:
     def out_ptrs(self):
         return [o.data_ptr() for o in self.outputs]
 
+    def calibrate_partition(self, modes=(0, 1), runs=7, rho=None):
+        """Runtime-aware choice of the SM-partition rule (MT_OPT_PARTITION) for this mix: time
+        the given schedule (default all-concurrent) under each rule, keep the fastest (median
+        of `runs` device makespans).  The paper's cost is measured latency (P:92-93, P:441);
+        the rule's own latency model is only an estimate (R16b)."""
+        from .mt import MT_OPT_PARTITION
+        if rho is None:
+            rho = [[] for _ in self.graphs]
+        self.ctx.set_schedule_pointers(rho)
+        med = {}
+        for m in modes:
+            self.ctx.set_option(MT_OPT_PARTITION, m)
+            self.run()
+            med[m] = float(np.median([self.run()[0] for _ in range(runs)]))
+        best = min(med, key=med.get)
+        self.ctx.set_option(MT_OPT_PARTITION, best)
+        self.partition = best
+        return best, med
+
     def run(self, stream=0):
         return self.ctx.run(self.in_ptrs, self.out_ptrs, stream)
 

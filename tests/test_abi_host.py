@@ -166,9 +166,21 @@ def test_op_cost_and_sm_partition_match_oracle(config):
         if st[0] != ir.E_OK:
             continue
         c.set_schedule_pointers(rho)
+        c.set_option(mt.MT_OPT_PARTITION, 0)      # roofline-proportional (north star)
         got = c.sm_partition().tolist()
         exp = [ir.sm_partition(w, 148) for w in ir.stage_weights(graphs, ranges, eb_of)]
         assert got == exp
+        for mode in (1, 2):                        # latency-balanced (R16b)
+            c.set_option(mt.MT_OPT_PARTITION, mode)
+            got = c.sm_partition().tolist()
+            exp = [ir.sm_partition_balanced([None if b == e else
+                                             [it for j in range(b, e) for it in c.op_work(t, j)]
+                                             for t, (b, e) in enumerate(st)], 148, mode) for st in ranges]
+            assert got == exp
+    for t, g in enumerate(graphs):
+        for j in range(g.n_ops):
+            w = c.op_work(t, j)
+            assert sum(k for k, _ in w) == c.op_tiles(t, j) and all(ns > 0 for _, ns in w)
 
 
 def test_zoo_graphs_ingest_and_reject_bad_graphs():

@@ -168,3 +168,59 @@ def test_sm_partition_invariants_and_hand_examples():
                 if W:
                     ideal = 1 + (148 - len(act)) * w[t] / W
                     assert abs(out[t] - ideal) < 1.0 + 1e-9
+
+
+def _E(items, t, n, mode, hop=2000):
+    if mode == 2:   # Brent: work / n + span
+        return -(-sum(k * ns for k, ns in items[t]) // n) + sum(ns + hop for _, ns in items[t])
+    return sum(-(-k // n) * ns for k, ns in items[t])
+
+
+def _minimax_brute(items, n_sms, mode=1):
+    """exhaustive optimum of max_t E_t(n_t) over every split of n_sms (each active tenant >= 1)"""
+    act = [t for t in range(len(items)) if items[t] is not None]
+
+    def E(t, n):
+        return _E(items, t, n, mode)
+
+    best = None
+
+    def rec(i, left, acc):
+        nonlocal best
+        if i == len(act) - 1:
+            v = max(acc + [E(act[i], left)])
+            best = v if best is None else min(best, v)
+            return
+        for n in range(1, left - (len(act) - 1 - i) + 1):
+            rec(i + 1, left - n, acc + [E(act[i], n)])
+
+    rec(0, n_sms, [])
+    return best
+
+
+def test_sm_partition_balanced_is_the_minimax_optimum():
+    """R16b: greedy 'feed the current maximum' reaches the exact minimum over all splits of
+    max_t sum ceil(tiles/n_t)*ns (brute force on small instances), keeps the invariants, and
+    reduces to an even split for identical tenants."""
+    import random
+    rnd = random.Random(11)
+    assert ir.sm_partition_balanced([[(100, 10)], [(100, 10)]], 10) == [5, 5]
+    # one long chain of 1-tile ops needs 1 CTA; the wide op gets the rest
+    assert ir.sm_partition_balanced([[(1, 1000)] * 5, [(64, 100)]], 9) == [1, 8]
+    assert ir.sm_partition_balanced([None, [(3, 1)], None], 7) == [0, 7, 0]
+    for _ in range(300):
+        n = rnd.randint(1, 4)
+        items = [None if rnd.random() < 0.2 else
+                 [(rnd.randint(1, 40), rnd.randint(1, 5000)) for _ in range(rnd.randint(1, 4))]
+                 for _ in range(n)]
+        act = [t for t in range(n) if items[t] is not None]
+        n_sms = rnd.randint(max(1, len(act)), 14)
+        for mode in (1, 2):
+            out = ir.sm_partition_balanced(items, n_sms, mode)
+            if not act:
+                assert out == [0] * n
+                continue
+            assert sum(out) == n_sms
+            assert all((out[t] >= 1) == (items[t] is not None) for t in range(n))
+            got = max(_E(items, t, out[t], mode) for t in act)
+            assert got == _minimax_brute(items, n_sms, mode)

@@ -22,6 +22,8 @@ ap.add_argument("--schedule", default="all_concurrent")
 ap.add_argument("--baseline", default=None)
 ap.add_argument("--out", default=None)
 ap.add_argument("--top", type=int, default=30)
+ap.add_argument("--partition", type=int, default=None)
+ap.add_argument("--steal", type=int, default=None)
 ap.add_argument("--synthetic", default=None, help="dwchain | pwchain | gapchain")
 a = ap.parse_args()
 if a.synthetic and a.synthetic.startswith("pw:"):
@@ -63,6 +65,11 @@ m.set_input(zoo.make_input(g[0]))
 rho = {"all_concurrent": configs.all_concurrent_pointers, "sequential": configs.sequential_pointers,
        "uniform4": configs.uniform_pointers}[a.schedule](L)
 m.ctx.set_schedule_pointers(rho)
+if a.partition is not None:
+    m.ctx.set_option(5, a.partition)
+if a.steal is not None:
+    m.ctx.set_option(1, a.steal)
+print("sm partition", m.ctx.sm_partition().tolist())
 for _ in range(3):
     m.run()
 cap = 1 << 16
