@@ -183,15 +183,16 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    def same_rule(m):
-        """every rank uses rank 0's measured partition rule (comparable latencies across ranks)"""
-        rule, med = m.calibrate_partition()
+    def same_knobs(m):
+        """measured executor knobs (partition rule, claim depth); every rank uses rank 0's choice
+        so latencies stay comparable across ranks"""
+        kn, med = m.calibrate()
         if ws > 1:
-            t = torch.tensor([rule], dtype=torch.int64, device=dev)
+            t = torch.tensor(list(kn), dtype=torch.int64, device=dev)
             dist.broadcast(t, 0)
-            rule = int(t.item())
-            m.ctx.set_option(5, rule)
-        return rule, med
+            kn = tuple(int(v) for v in t.tolist())
+            m.set_knobs(kn)
+        return kn, med
 
     graphs = configs.tenants(args.config)
     L = [g.n_ops for g in graphs]
@@ -215,7 +216,7 @@ def main():
         return [a.elapsed_time(b) for a, b in evs]
 
     # ---- SM-partition rule chosen by measurement (outside the timed region) ----
-    part_rule, part_med = same_rule(mix)
+    knobs, knob_med = same_knobs(mix)
     # ---- schedule search (outside the timed region): profile candidates, keep the best ----
     cands = configs.sample_candidates(L, args.search_cand, seed=14255)
     named = {"all_concurrent": configs.all_concurrent_pointers(L),
@@ -294,7 +295,7 @@ def main():
         PL = [g.n_ops for g in pg]
         allc = configs.sample_candidates(PL, args.n_cand, seed=14255)
         from paper_2111_14255_b200 import distributed as D
-        prule, _ = same_rule(pmix)
+        pknobs, _ = same_knobs(pmix)
         pfn = lambda cs: pmix.ctx.profile_batch_pointers(cs, pmix.in_ptrs, pmix.out_ptrs, 2, 10, sp)
         pmix.ctx.profile_batch_pointers(allc[:8], pmix.in_ptrs, pmix.out_ptrs, 1, 1, sp)  # warm
         barrier()
@@ -314,7 +315,7 @@ def main():
                            "best_us": cdr.best_lat, "start_us": cdr.records[0][1],
                            "wall_s": time.perf_counter() - t1}
         prof_line = {"config": args.profile_config, "candidates": args.n_cand, "warmup": 2, "iters": 10,
-                     "sm_partition_rule": prule,
+                     "knobs": {"sm_partition_rule": pknobs[0], "claim_depth": pknobs[1]},
                      "schedules_per_s": args.n_cand / dt, "wall_s": dt,
                      "feasible": int((st_p == 0).sum()),
                      "best_us": float(np.nanmin(lat_p)) if len(lat_p) else None,
@@ -340,7 +341,8 @@ def main():
                                    + configs.CONFIGS[args.config][3],
                        "schedule": head_name, "stages": n_stages,
                        "sm_partition_rule": {0: "roofline-proportional", 1: "latency-balanced",
-                                             2: "work/span"}[part_rule],
+                                             2: "work/span"}[knobs[0]],
+                       "claim_depth": knobs[1],
                        "l2": "warm" if args.warm_l2 else "flushed before every timed step (256 MiB write)",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
             "gpu_launches": K,

@@ -119,12 +119,16 @@ typedef enum {
   MT_OPT_NUM_SMS = 2,      /* host-only contexts: SM count used for the partition (148)    */
   MT_OPT_TIMEOUT_MS = 3,   /* device spin timeout (default 2000 ms)                         */
   MT_OPT_CTAS_PER_SM = 4,  /* reserved (1)                                                  */
-  MT_OPT_PARTITION = 5     /* SM partition rule per stage (a3; R16 / R16b):       */
+  MT_OPT_PARTITION = 5,    /* SM partition rule per stage (a3; R16 / R16b):       */
                            /* 0 (default): n_t proportional to the slice's roofline time    */
                            /*    (north star); 1: latency-balanced -- minimise max_t E_t,   */
                            /*    E_t(n) = sum over the slice's work items ceil(tiles/n)*ns  */
                            /*    (mt_op_work); 2: work/span, E_t(n) = ceil(W_t/n) + S_t.    */
                            /*    Setting it re-plans the active schedule.                   */
+  MT_OPT_CLAIM_DEPTH = 6   /* 0 (default): a CTA may claim any tile of its tenant's slice     */
+                           /* (claim-then-wait); D >= 1: a tile of op o is claimable only   */
+                           /* once op o-D of the same slice is complete (bounded claim-ahead:*/
+                           /* CTAs blocked everywhere retry instead of parking on a tile)   */
 } mt_option;
 
 /* execution modes of mt_run_baseline: the same tile functions launched one kernel per op */

@@ -28,6 +28,7 @@ struct mt_ctx {
   int n_sms = 148;
   int grid = 148;
   int steal = 2;
+  int claim_depth = 0; // MT_OPT_CLAIM_DEPTH
   int partition = 0;   // MT_OPT_PARTITION: 0 roofline-proportional, 1 latency-balanced, 2 work/span
   int64_t timeout_ms = 2000;
   bool loaded = false, bound = false, has_sched = false;
@@ -757,6 +758,7 @@ static RunArgs base_args(mt_ctx *c, const float *const *inputs, float *const *ou
   a.n_stages = c->has_sched ? c->sched.S : 0;
   a.n_tenants = N;
   a.steal = c->steal;
+  a.claim_depth = c->claim_depth;
   a.claim = (int32_t *)(c->ws + c->lay.claim);
   a.done = (int32_t *)(c->ws + c->lay.done);
   a.blkcnt = (int32_t *)(c->ws + c->lay.blk);
@@ -965,6 +967,10 @@ mt_status mt_set_option(mt_ctx *c, int32_t option, int64_t value) {
       c->timeout_ms = value;
       return MT_OK;
     case MT_OPT_CTAS_PER_SM: return value == 1 ? MT_OK : fail(c, MT_ERR_ARG, "only 1 CTA/SM");
+    case MT_OPT_CLAIM_DEPTH:
+      if (value < 0 || value > 1 << 20) return fail(c, MT_ERR_ARG, "bad claim depth");
+      c->claim_depth = (int)value;
+      return MT_OK;
     case MT_OPT_PARTITION:
       if (value < 0 || value > 2) return fail(c, MT_ERR_ARG, "partition must be 0, 1 or 2");
       c->partition = (int)value;

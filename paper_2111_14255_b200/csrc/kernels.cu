@@ -38,7 +38,7 @@ struct CtaShared {
   unsigned long long t_pick, t_pick_next, t_deps, t_mma, t_run, t_first, t_lastmma, t_aissue;
   unsigned long long t_kb[4], t_is[1];
   int *xrel;   // extra counter released with the tile (split-K partial arrival)
-  int cur[MT_MAXT], end[MT_MAXT];
+  int cur[MT_MAXT], end[MT_MAXT], beg[MT_MAXT];
   uint32_t complete[64];      // bitset of ops observed fully complete (global op id < 2048)
   float esc[128], esh[128];   // epilogue scale / shift of the current conv tile's columns
   OpDesc d;
@@ -1686,7 +1686,7 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int t = 0; t < T; ++t) {
-      sh.cur[t] = a.rng[(s * T + t) * 2];
+      sh.beg[t] = sh.cur[t] = a.rng[(s * T + t) * 2];
       sh.end[t] = a.rng[(s * T + t) * 2 + 1];
     }
     sh.home = a.home[(size_t)s * gridDim.x + blockIdx.x];
@@ -1700,6 +1700,7 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
       // the most unclaimed ops of its slice first (critical-path-first list scheduling)
       // (selection on the fly, no local array: ties go to the earlier tenant in round-robin order)
       unsigned visited = 0;
+      bool blocked = false;   // claim_depth: some tenant has unclaimed tiles not yet claimable
       for (int q = 0; q < T && op < 0; ++q) {
         if (!a.steal && q > 0) break;
         int t = sh.home + q;
@@ -1717,10 +1718,27 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
         visited |= 1u << t;
         while (sh.cur[t] < sh.end[t]) {
           const int o = sh.cur[t];
+          if (a.claim_depth > 0 && o - a.claim_depth >= sh.beg[t]) {
+            // bounded claim-ahead: op o is claimable once op o - D is complete (ops before the
+            // stage are complete by the barrier), so CTAs do not park on tiles far down a
+            // latency-bound chain while other tenants have ready work
+            const int x = o - a.claim_depth;
+            bool cpl = x < 2048 && ((sh.complete[x >> 5] >> (x & 31)) & 1u);
+            if (!cpl && ld_acquire(a.done + x) >= __ldg(&a.ops[x].tiles)) {
+              cpl = true;
+              if (x < 2048) atomicOr(&sh.complete[x >> 5], 1u << (x & 31));
+            }
+            if (!cpl) { blocked = true; break; }
+          }
           const int k = atomicAdd(a.claim + o, 1);
           if (k < __ldg(&a.ops[o].tiles)) { op = o; tile = k; ten = t; break; }
           sh.cur[t] = o + 1;  // every tile of o is claimed
         }
+      }
+      if (op < 0 && blocked) {   // work remains but none is claimable yet: retry shortly
+        op = -2;
+        if (ld_acquire_u(&a.ctl->error)) op = -3;
+        __nanosleep(100);
       }
       sh.op = op;
       sh.tile = tile;
@@ -1730,6 +1748,8 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
     __syncthreads();
     const int op = sh.op;
     const int my_tile = sh.tile;
+    if (op == -2) continue;
+    if (op == -3) return false;
     if (op < 0) return true;
     if (tid == 0) {
       sh.t_pick = sh.t_pick_next;

@@ -86,6 +86,7 @@ struct RunArgs {
   const int32_t *rng;        // [S][T][2] global op ids (begin, end)
   const uint8_t *home;       // [S][grid] home tenant of each CTA
   int32_t n_stages, n_tenants, steal, n_pack;
+  int32_t claim_depth;       // 0: claim any tile of the slice; D: only ops whose op D earlier is complete
   int32_t *claim;            // [n_ops] tile claim counters
   int32_t *done;             // [n_ops] completed-tile counters
   int32_t *blkcnt;           // [total blocks] completed-tile counters per output pixel block

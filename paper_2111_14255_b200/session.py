@@ -53,24 +53,35 @@ class TenantMix:
     def out_ptrs(self):
         return [o.data_ptr() for o in self.outputs]
 
-    def calibrate_partition(self, modes=(0, 1), runs=7, rho=None):
-        """Runtime-aware choice of the SM-partition rule (MT_OPT_PARTITION) for this mix: time
-        the given schedule (default all-concurrent) under each rule, keep the fastest (median
-        of `runs` device makespans).  The paper's cost is measured latency (P:92-93, P:441);
-        the rule's own latency model is only an estimate (R16b)."""
-        from .mt import MT_OPT_PARTITION
+    # (partition rule, claim depth) pairs tried by calibrate(): the roofline rule of the north
+    # star, the latency-balanced rule (R16b), each with unbounded and bounded claim-ahead
+    KNOBS = ((0, 0), (1, 0), (0, 3), (1, 3), (1, 5))
+
+    def calibrate(self, knobs=KNOBS, runs=7, rho=None):
+        """Runtime-aware choice of the executor's scheduling knobs for this mix: the SM-partition
+        rule (MT_OPT_PARTITION) and the claim-ahead depth (MT_OPT_CLAIM_DEPTH).  Times the given
+        schedule (default all-concurrent) under each (rule, depth) pair and keeps the fastest
+        (median of `runs` device makespans) -- the paper's cost is measured latency (P:92-93,
+        P:441); the knobs change which CTA runs a tile and when, never the outputs."""
+        from .mt import MT_OPT_CLAIM_DEPTH, MT_OPT_PARTITION
         if rho is None:
             rho = [[] for _ in self.graphs]
         self.ctx.set_schedule_pointers(rho)
         med = {}
-        for m in modes:
-            self.ctx.set_option(MT_OPT_PARTITION, m)
+        for k in knobs:
+            self.ctx.set_option(MT_OPT_PARTITION, k[0])
+            self.ctx.set_option(MT_OPT_CLAIM_DEPTH, k[1])
             self.run()
-            med[m] = float(np.median([self.run()[0] for _ in range(runs)]))
+            med[tuple(k)] = float(np.median([self.run()[0] for _ in range(runs)]))
         best = min(med, key=med.get)
-        self.ctx.set_option(MT_OPT_PARTITION, best)
-        self.partition = best
+        self.set_knobs(best)
         return best, med
+
+    def set_knobs(self, knobs):
+        from .mt import MT_OPT_CLAIM_DEPTH, MT_OPT_PARTITION
+        self.ctx.set_option(MT_OPT_PARTITION, knobs[0])
+        self.ctx.set_option(MT_OPT_CLAIM_DEPTH, knobs[1])
+        self.knobs = tuple(knobs)
 
     def run(self, stream=0):
         return self.ctx.run(self.in_ptrs, self.out_ptrs, stream)

@@ -230,3 +230,23 @@ def test_op_plans_follow_the_operand_rules():
             if nd["kind"] == 7:   # FC
                 p = c8.op_plan(t, j)
                 assert p["kind"] == "conv_tc" and p["path"] == 3, (g.name, j, p)
+
+
+def test_scheduling_knob_options_validated():
+    """MT_OPT_PARTITION in {0,1,2} re-plans the active schedule; MT_OPT_CLAIM_DEPTH >= 0;
+    anything else is MT_ERR_ARG and leaves the previous value (R16b, R20)."""
+    graphs = configs.tenants("c2")
+    c = host_ctx(graphs)
+    L = [g.n_ops for g in graphs]
+    c.set_schedule_pointers(configs.all_concurrent_pointers(L))
+    c.set_option(mt.MT_OPT_PARTITION, 0)
+    p0 = c.sm_partition().tolist()
+    c.set_option(mt.MT_OPT_PARTITION, 1)
+    p1 = c.sm_partition().tolist()
+    assert p0 != p1 and sum(p1[0]) == 148
+    for opt, bad in ((mt.MT_OPT_PARTITION, 3), (mt.MT_OPT_PARTITION, -1), (mt.MT_OPT_CLAIM_DEPTH, -1)):
+        with pytest.raises(Exception):
+            c.set_option(opt, bad)
+    assert c.sm_partition().tolist() == p1
+    for d in (0, 1, 3, 100):
+        c.set_option(mt.MT_OPT_CLAIM_DEPTH, d)

@@ -137,6 +137,32 @@ def test_steal_off_same_outputs():
         assert torch.equal(a, b)
 
 
+def test_partition_rules_and_claim_depth_same_outputs():
+    """Partition rules (R16/R16b) and bounded claim-ahead change only which CTA runs a tile and
+    when: outputs stay bit-identical (c3: three tenants, split-K convs, tensor-core FC)."""
+    from paper_2111_14255_b200 import mt as M
+    m = mix_for("c3")
+    L = [g.n_ops for g in m.graphs]
+    for rho in (configs.all_concurrent_pointers(L), configs.uniform_pointers(L)):
+        m.ctx.set_schedule_pointers(rho)
+        m.ctx.set_option(M.MT_OPT_PARTITION, 0)
+        m.ctx.set_option(M.MT_OPT_CLAIM_DEPTH, 0)
+        m.run()
+        ref = _outs(m)
+        for part, steal, depth in ((1, 2, 0), (2, 2, 0), (0, 2, 2), (1, 2, 3), (0, 0, 2), (1, 1, 1)):
+            m.ctx.set_option(M.MT_OPT_PARTITION, part)
+            m.ctx.set_option(M.MT_OPT_STEAL, steal)
+            m.ctx.set_option(M.MT_OPT_CLAIM_DEPTH, depth)
+            for o in m.outputs:
+                o.zero_()
+            m.run()
+            for a, b in zip(_outs(m), ref):
+                assert torch.equal(a, b), (rho, part, steal, depth)
+    m.ctx.set_option(M.MT_OPT_PARTITION, 0)
+    m.ctx.set_option(M.MT_OPT_STEAL, 2)
+    m.ctx.set_option(M.MT_OPT_CLAIM_DEPTH, 0)
+
+
 def test_profile_batch_statuses_and_latencies():
     m = mix_for("c2")
     L = [g.n_ops for g in m.graphs]

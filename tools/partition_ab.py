@@ -18,7 +18,7 @@ from workloads import configs, zoo  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="c2,c3,c4")
 ap.add_argument("--runs", type=int, default=30)
-ap.add_argument("--modes", default="0:2,1:2", help="partition:steal pairs")
+ap.add_argument("--modes", default="0:2,1:2", help="partition:steal[:claim_depth] tuples")
 ap.add_argument("--out", default=None)
 a = ap.parse_args()
 modes = [tuple(int(v) for v in m.split(":")) for m in a.modes.split(",")]
@@ -37,11 +37,14 @@ for cfg in a.configs.split(","):
             for md in (modes if rep % 2 == 0 else modes[::-1]):
                 m.ctx.set_option(mt.MT_OPT_PARTITION, md[0])
                 m.ctx.set_option(mt.MT_OPT_STEAL, md[1])
+                m.ctx.set_option(mt.MT_OPT_CLAIM_DEPTH, md[2] if len(md) > 2 else 0)
                 if rep == 0:
                     for _ in range(3):
                         m.run()
                 ts[md].append(m.run()[0])
-        row = {f"p{md[0]}s{md[1]}": round(statistics.median(v), 1) for md, v in ts.items()}
+        row = {"p%ds%d" % md[:2] + ("d%d" % md[2] if len(md) > 2 else ""): round(statistics.median(v), 1)
+               for md, v in ts.items()}
+        m.ctx.set_option(mt.MT_OPT_CLAIM_DEPTH, 0)
         m.ctx.set_option(mt.MT_OPT_PARTITION, 1)
         row["sms_balanced"] = m.ctx.sm_partition().tolist()
         m.ctx.set_option(mt.MT_OPT_PARTITION, 0)
