@@ -126,8 +126,9 @@ typedef enum {
                            /*    (mt_op_work); 2: work/span, E_t(n) = ceil(W_t/n) + S_t.    */
                            /*    Setting it re-plans the active schedule.                   */
   MT_OPT_CLAIM_DEPTH = 6   /* 0 (default): a CTA may claim any tile of its tenant's slice     */
-                           /* (claim-then-wait); D >= 1: a tile of op o is claimable only   */
-                           /* once op o-D of the same slice is complete (bounded claim-ahead:*/
+                           /* (claim-then-wait).  D > 0: a tile of op o is claimable only   */
+                           /* once o's ancestors at DAG distance D are complete; D < 0: once */
+                           /* op o-|D| of the same tenant is complete (bounded claim-ahead: */
                            /* CTAs blocked everywhere retry instead of parking on a tile)   */
 } mt_option;
 

@@ -634,6 +634,7 @@ static mt_status plan_graphs(mt_ctx *c) {
   L.ctl = take(sizeof(CtlBlock));
   L.claim = take(sizeof(int32_t) * total);
   L.done = take(sizeof(int32_t) * total);
+  L.gates = take(sizeof(int32_t) * total);
   L.blk = take(sizeof(int32_t) * std::max(c->total_blocks, 1));
   L.splitcnt = take(sizeof(int32_t) * std::max(split_cnt, 1));
   L.counters_bytes = off;
@@ -674,6 +675,41 @@ static std::vector<int> lengths(mt_ctx *c) {
   std::vector<int> L;
   for (auto &t : c->T) L.push_back(t.L);
   return L;
+}
+
+// Gate op of every op for claim depth D (R20), -1 = none.  D > 0: the newest (largest
+// id) of o's ancestors at DAG distance exactly D (layer D of a breadth-first walk up the dependency
+// edges; older members of the layer complete first).  D < 0: op o - |D| of the same tenant.  No
+// gate when o is closer than |D| to the graph input.  Any ancestor keeps claiming deadlock-free.
+static std::vector<int32_t> gate_table(mt_ctx *c, int D) {
+  const int n = (int)c->ops.size();
+  std::vector<int32_t> g((size_t)n, -1);
+  if (D == 0) return g;
+  for (int o = 0; o < n; ++o) {
+    if (D < 0) {
+      if (o + D >= c->T[c->ops[o].d.tenant].op_base) g[o] = o + D;
+      continue;
+    }
+    std::vector<int> layer{o};
+    for (int k = 1; k <= D && !layer.empty(); ++k) {
+      std::vector<int> nx;
+      for (int x : layer) {
+        const OpDesc &d = c->ops[x].d;
+        for (int r = 0; r < d.n_dep; ++r)
+          if (std::find(nx.begin(), nx.end(), d.deps[r]) == nx.end()) nx.push_back(d.deps[r]);
+      }
+      layer = nx;
+    }
+    for (int x : layer) g[o] = std::max(g[o], x);
+  }
+  return g;
+}
+
+static mt_status upload_gates(mt_ctx *c) {
+  if (c->host_only || !c->bound) return MT_OK;
+  std::vector<int32_t> g = gate_table(c, c->claim_depth);
+  CK(cudaMemcpy(c->ws + c->lay.gates, g.data(), g.size() * 4, cudaMemcpyHostToDevice));
+  return MT_OK;
 }
 
 static void build_stage_plan(mt_ctx *c, Schedule &s) {
@@ -758,7 +794,8 @@ static RunArgs base_args(mt_ctx *c, const float *const *inputs, float *const *ou
   a.n_stages = c->has_sched ? c->sched.S : 0;
   a.n_tenants = N;
   a.steal = c->steal;
-  a.claim_depth = c->claim_depth;
+  a.claim_depth = (int)c->ops.size() <= MT_GATE_OPS ? c->claim_depth : 0;
+  a.gates = (const int32_t *)(c->ws + c->lay.gates);
   a.claim = (int32_t *)(c->ws + c->lay.claim);
   a.done = (int32_t *)(c->ws + c->lay.done);
   a.blkcnt = (int32_t *)(c->ws + c->lay.blk);
@@ -968,9 +1005,11 @@ mt_status mt_set_option(mt_ctx *c, int32_t option, int64_t value) {
       return MT_OK;
     case MT_OPT_CTAS_PER_SM: return value == 1 ? MT_OK : fail(c, MT_ERR_ARG, "only 1 CTA/SM");
     case MT_OPT_CLAIM_DEPTH:
-      if (value < 0 || value > 1 << 20) return fail(c, MT_ERR_ARG, "bad claim depth");
+      if (value < -(1 << 20) || value > 1 << 20) return fail(c, MT_ERR_ARG, "bad claim depth");
+      if (value != 0 && c->loaded && (int)c->ops.size() > MT_GATE_OPS)
+        return fail(c, MT_ERR_ARG, "claim depth needs <= 2048 ops in the mix");
       c->claim_depth = (int)value;
-      return MT_OK;
+      return upload_gates(c);
     case MT_OPT_PARTITION:
       if (value < 0 || value > 2) return fail(c, MT_ERR_ARG, "partition must be 0, 1 or 2");
       c->partition = (int)value;
@@ -1123,6 +1162,7 @@ mt_status mt_bind_workspace(mt_ctx *c, void *dev, size_t bytes) {
   }
   CK(cudaDeviceSynchronize());
   c->bound = true;
+  if (upload_gates(c) != MT_OK) return c->err.st;
   if (c->has_sched) return apply_schedule(c, c->sched);
   return MT_OK;
 }

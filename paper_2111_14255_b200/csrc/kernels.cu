@@ -40,6 +40,7 @@ struct CtaShared {
   int *xrel;   // extra counter released with the tile (split-K partial arrival)
   int cur[MT_MAXT], end[MT_MAXT], beg[MT_MAXT];
   uint32_t complete[64];      // bitset of ops observed fully complete (global op id < 2048)
+  int16_t gate[MT_GATE_OPS];  // claim-ahead gate op of each op (-1 none; claim_depth != 0)
   float esc[128], esh[128];   // epilogue scale / shift of the current conv tile's columns
   OpDesc d;
 };
@@ -67,6 +68,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ int ld_acquire(const int *p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_relaxed(const int *p) {   // heuristic reads: no ordering needed
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ unsigned ld_acquire_u(const unsigned *p) {
@@ -817,6 +823,8 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
   const int m = conv_row_pixel(d, ct, r);
   const int hcols = d.bn >> 1;
   const uint32_t tl = sh.tmem_base + ((uint32_t)(32 * q) << 16);
+  const bool stamp = a.trace != nullptr && (tid == 0 || tid == 255);
+  if (stamp) sh.t_kb[tid == 0 ? 0 : 2] = gtimer();   // epilogue start (warp 0 / warp 7)
   if (S == 1) {
     if (hcols >= 32) {
       for (int cb = half * hcols; cb < (half + 1) * hcols; cb += 32) {
@@ -911,6 +919,7 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
     // published together with the tile's completion in run_stage (one fence for all counters)
     if (tid == 0) sh.xrel = a.splitcnt + d.cnt_off + tmn;
   }
+  if (stamp) sh.t_kb[tid == 0 ? 1 : 3] = gtimer();   // stores issued (warp 0 / warp 7)
   tc_fence_before();
   __syncthreads();
 }
@@ -1718,15 +1727,17 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
         visited |= 1u << t;
         while (sh.cur[t] < sh.end[t]) {
           const int o = sh.cur[t];
-          if (a.claim_depth > 0 && o - a.claim_depth >= sh.beg[t]) {
-            // bounded claim-ahead: op o is claimable once op o - D is complete (ops before the
-            // stage are complete by the barrier), so CTAs do not park on tiles far down a
-            // latency-bound chain while other tenants have ready work
-            const int x = o - a.claim_depth;
-            bool cpl = x < 2048 && ((sh.complete[x >> 5] >> (x & 31)) & 1u);
-            if (!cpl && ld_acquire(a.done + x) >= __ldg(&a.ops[x].tiles)) {
+          if (a.claim_depth != 0) {
+            // bounded claim-ahead: op o is claimable once its gate op (host table, staged in
+            // shared memory: an ancestor at DAG distance D, or op o - |D|) is complete, so CTAs do
+            // not park on tiles far down a latency-bound chain while other tenants have ready
+            // work.  Relaxed read: a claiming heuristic; the tile's own dependency wait
+            // (acquire) orders its data reads.
+            const int x = sh.gate[o];
+            bool cpl = x < 0 || ((sh.complete[x >> 5] >> (x & 31)) & 1u);
+            if (!cpl && ld_relaxed(a.done + x) >= __ldg(&a.ops[x].tiles)) {
               cpl = true;
-              if (x < 2048) atomicOr(&sh.complete[x >> 5], 1u << (x & 31));
+              atomicOr(&sh.complete[x >> 5], 1u << (x & 31));
             }
             if (!cpl) { blocked = true; break; }
           }
@@ -1858,6 +1869,8 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
   PipeState ps{0u, 0u, 0u};
   if (threadIdx.x < 64) sh.complete[threadIdx.x] = 0u;
   if (threadIdx.x == 0) sh.smem_cap = PIPE_BYTES;
+  if (a.claim_depth != 0)
+    for (int i = threadIdx.x; i < a.n_ops; i += blockDim.x) sh.gate[i] = (int16_t)__ldg(a.gates + i);
   cta_setup(sh, true);
   bool ok = grid_barrier(a, sh);
   if (ok) {

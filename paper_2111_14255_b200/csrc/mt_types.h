@@ -18,6 +18,7 @@
 #define MT_EW_PER_THREAD 2   // 8-channel vectors per thread in pointwise tiles
 #define MT_FC_ROWS 8         // FC output rows per tile (one per warp)
 #define MT_FC_BATCH 8        // FC batch columns per pass
+#define MT_GATE_OPS 2048     // bounded claim-ahead: gate table staged in shared memory (ops)
 
 enum mt_tile_kind {
   TK_NONE = 0,
@@ -86,7 +87,8 @@ struct RunArgs {
   const int32_t *rng;        // [S][T][2] global op ids (begin, end)
   const uint8_t *home;       // [S][grid] home tenant of each CTA
   int32_t n_stages, n_tenants, steal, n_pack;
-  int32_t claim_depth;       // 0: claim any tile of the slice; D: only ops whose op D earlier is complete
+  int32_t claim_depth;       // 0: claim any tile of the slice; D: only ops whose gate ops are complete
+  const int32_t *gates;      // [n_ops]: gate op of each op (-1 none), host table for claim_depth
   int32_t *claim;            // [n_ops] tile claim counters
   int32_t *done;             // [n_ops] completed-tile counters
   int32_t *blkcnt;           // [total blocks] completed-tile counters per output pixel block

@@ -57,6 +57,7 @@ struct Schedule {
 };
 
 struct Layout {
+  size_t gates = 0;   // [n_ops]: claim-ahead gate op (-1 none), MT_OPT_CLAIM_DEPTH
   size_t ctl = 0, claim = 0, done = 0, blk = 0, splitcnt = 0, ops = 0, tmaps = 0, sched_rng = 0, sched_home = 0,
          prof_area = 0, prof_ts = 0, run_ts = 0, packed = 0, stage_in = 0, stage_out = 0,
          weights = 0, acts = 0, partials = 0, total = 0;

@@ -55,7 +55,7 @@ class TenantMix:
 
     # (partition rule, claim depth) pairs tried by calibrate(): the roofline rule of the north
     # star, the latency-balanced rule (R16b), each with unbounded and bounded claim-ahead
-    KNOBS = ((0, 0), (1, 0), (0, 3), (1, 3), (1, 5))
+    KNOBS = ((0, 0), (1, 0), (1, 2), (1, 3), (0, 3))
 
     def calibrate(self, knobs=KNOBS, runs=7, rho=None):
         """Runtime-aware choice of the executor's scheduling knobs for this mix: the SM-partition

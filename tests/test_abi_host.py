@@ -244,9 +244,9 @@ def test_scheduling_knob_options_validated():
     c.set_option(mt.MT_OPT_PARTITION, 1)
     p1 = c.sm_partition().tolist()
     assert p0 != p1 and sum(p1[0]) == 148
-    for opt, bad in ((mt.MT_OPT_PARTITION, 3), (mt.MT_OPT_PARTITION, -1), (mt.MT_OPT_CLAIM_DEPTH, -1)):
+    for opt, bad in ((mt.MT_OPT_PARTITION, 3), (mt.MT_OPT_PARTITION, -1), (mt.MT_OPT_CLAIM_DEPTH, 1 << 21)):
         with pytest.raises(Exception):
             c.set_option(opt, bad)
     assert c.sm_partition().tolist() == p1
-    for d in (0, 1, 3, 100):
+    for d in (0, 1, 3, 100, -3):
         c.set_option(mt.MT_OPT_CLAIM_DEPTH, d)

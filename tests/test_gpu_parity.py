@@ -161,6 +161,20 @@ def test_partition_rules_and_claim_depth_same_outputs():
     m.ctx.set_option(M.MT_OPT_PARTITION, 0)
     m.ctx.set_option(M.MT_OPT_STEAL, 2)
     m.ctx.set_option(M.MT_OPT_CLAIM_DEPTH, 0)
+    # Inception's branches: DAG-distance gates (several gate ops per concat consumer)
+    m = mix_for("c4")
+    L = [g.n_ops for g in m.graphs]
+    m.ctx.set_schedule_pointers(configs.all_concurrent_pointers(L))
+    m.run()
+    ref = _outs(m)
+    for depth in (2, 3, 1):
+        m.ctx.set_option(M.MT_OPT_CLAIM_DEPTH, depth)
+        for o in m.outputs:
+            o.zero_()
+        m.run()
+        for a, b in zip(_outs(m), ref):
+            assert torch.equal(a, b), depth
+    m.ctx.set_option(M.MT_OPT_CLAIM_DEPTH, 0)
 
 
 def test_profile_batch_statuses_and_latencies():

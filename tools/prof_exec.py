@@ -18,7 +18,8 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--schedule", default="all_concurrent")
 ap.add_argument("--runs", type=int, default=5)
 ap.add_argument("--baseline", default=None)
-ap.add_argument("--steal", type=int, default=1)
+ap.add_argument("--steal", type=int, default=2)
+ap.add_argument("--knobs", default="0,0", help="partition rule, claim depth (TenantMix.calibrate)")
 a = ap.parse_args()
 g = configs.tenants(a.config)
 L = [x.n_ops for x in g]
@@ -27,6 +28,7 @@ m.set_input(zoo.make_input(g[0]))
 rho = {"all_concurrent": configs.all_concurrent_pointers, "sequential": configs.sequential_pointers,
        "uniform4": configs.uniform_pointers}[a.schedule](L)
 m.ctx.set_schedule_pointers(rho)
+m.set_knobs(tuple(int(v) for v in a.knobs.split(",")))
 for i in range(a.runs):
     if a.baseline:
         us = m.ctx.run_baseline(a.baseline, m.in_ptrs, m.out_ptrs)

@@ -24,6 +24,7 @@ ap.add_argument("--out", default=None)
 ap.add_argument("--top", type=int, default=30)
 ap.add_argument("--partition", type=int, default=None)
 ap.add_argument("--steal", type=int, default=None)
+ap.add_argument("--claim", type=int, default=None)
 ap.add_argument("--synthetic", default=None, help="dwchain | pwchain | gapchain")
 a = ap.parse_args()
 if a.synthetic and a.synthetic.startswith("pw:"):
@@ -69,6 +70,8 @@ if a.partition is not None:
     m.ctx.set_option(5, a.partition)
 if a.steal is not None:
     m.ctx.set_option(1, a.steal)
+if a.claim is not None:
+    m.ctx.set_option(6, a.claim)
 print("sm partition", m.ctx.sm_partition().tolist())
 for _ in range(3):
     m.run()
