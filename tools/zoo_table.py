@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--runs", type=int, default=20)
     ap.add_argument("--cands", type=int, default=128)
     ap.add_argument("--out", default="gpurun_out/zoo_table.json")
+    ap.add_argument("--no-calibrate", action="store_true")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
@@ -68,6 +69,10 @@ def main():
         ctx = m.ctx
         run = lambda: ctx.run_async(m.in_ptrs, m.out_ptrs, sp)
         r = {"tenants": list(configs.CONFIGS[cfg][0]), "ops": L}
+        if not a.no_calibrate:   # executor knobs (partition rule, claim depth) chosen by measurement
+            kn, med = m.calibrate()
+            r["knobs"] = {"sm_partition_rule": kn[0], "claim_depth": kn[1],
+                          "calibration_us": {f"{k[0]},{k[1]}": round(v, 1) for k, v in med.items()}}
         for name, rho in (("all_concurrent", configs.all_concurrent_pointers(L)),
                           ("sequential_schedule", configs.sequential_pointers(L)),
                           ("uniform4", configs.uniform_pointers(L))):
@@ -90,7 +95,8 @@ def main():
         r["best_executor_ms"] = best_exec
         r["speedup_vs_seq"] = min(base["seq"], base["seq_graph"]) / best_exec
         r["speedup_vs_multistream"] = min(base["ms_dfs"], base["ms_bfs"], base["ms_graph"]) / best_exec
-        r["paper_context"] = dict(zip(("table", "cudnn_seq_ms", "stream_parallel_ms", "ours_c_ms"), PAPER[cfg]))
+        if cfg in PAPER:
+            r["paper_context"] = dict(zip(("table", "cudnn_seq_ms", "stream_parallel_ms", "ours_c_ms"), PAPER[cfg]))
         r["wall_s"] = time.time() - t0
         res[cfg] = r
         print(cfg, json.dumps({k: v for k, v in r.items() if k not in ("ops",)}), flush=True)
@@ -98,6 +104,27 @@ def main():
         torch.cuda.empty_cache()
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     json.dump(res, open(a.out, "w"), indent=1)
+    open(a.out.replace(".json", ".md"), "w").write(render_md(res) + "\n")
+
+
+
+def render_md(res):
+    """Markdown table of a zoo_table JSON (profiles/<round>_zoo_table.md body)."""
+    rows = ["| mix | knobs (rule, D) | all-conc. | rand | coord (P3,R2,M8) | seq sched. | SEQ | SEQ_G | MS_BFS | MS_G "
+            "| STAGE_EV | best vs SEQ_G | best vs MS_G | paper Seq / Stream / Ours-C |",
+            "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+    for cfg, r in res.items():
+        b = r["baselines"]
+        kn = r.get("knobs")
+        pc = r.get("paper_context")
+        paper = f"{pc['cudnn_seq_ms']} / {pc['stream_parallel_ms']} / {pc['ours_c_ms']} ({pc['table']})" if pc else "-"
+        rows.append(
+            f"| {cfg}: {'+'.join(r['tenants'])} | {(kn['sm_partition_rule'], kn['claim_depth']) if kn else '(0, 0)'} "
+            f"| {r['all_concurrent']:.3f} | {r['random_search']['ms']:.3f} | {r['coordinate_descent']['ms']:.3f} "
+            f"| {r['sequential_schedule']:.3f} | {b['seq']:.3f} | {b['seq_graph']:.3f} | {b['ms_bfs']:.3f} "
+            f"| {b['ms_graph']:.3f} | {b['stage_events']:.3f} | {min(b['seq'], b['seq_graph']) / r['best_executor_ms']:.2f}x "
+            f"| {min(b['ms_dfs'], b['ms_bfs'], b['ms_graph']) / r['best_executor_ms']:.2f}x | {paper} |")
+    return "\n".join(rows)
 
 
 if __name__ == "__main__":
