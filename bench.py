@@ -315,7 +315,8 @@ def main():
                            "best_us": cdr.best_lat, "start_us": cdr.records[0][1],
                            "wall_s": time.perf_counter() - t1}
         prof_line = {"config": args.profile_config, "candidates": args.n_cand, "warmup": 2, "iters": 10,
-                     "knobs": {"sm_partition_rule": pknobs[0], "claim_depth": pknobs[1]},
+                     "knobs": {"sm_partition_rule": pknobs[0], "claim_depth": pknobs[1],
+                               "steal": pknobs[2] if len(pknobs) > 2 else 2},
                      "schedules_per_s": args.n_cand / dt, "wall_s": dt,
                      "feasible": int((st_p == 0).sum()),
                      "best_us": float(np.nanmin(lat_p)) if len(lat_p) else None,
@@ -342,7 +343,7 @@ def main():
                        "schedule": head_name, "stages": n_stages,
                        "sm_partition_rule": {0: "roofline-proportional", 1: "latency-balanced",
                                              2: "work/span"}[knobs[0]],
-                       "claim_depth": knobs[1],
+                       "claim_depth": knobs[1], "steal": knobs[2] if len(knobs) > 2 else 2,
                        "l2": "warm" if args.warm_l2 else "flushed before every timed step (256 MiB write)",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
             "gpu_launches": K,

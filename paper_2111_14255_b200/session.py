@@ -53,24 +53,24 @@ class TenantMix:
     def out_ptrs(self):
         return [o.data_ptr() for o in self.outputs]
 
-    # (partition rule, claim depth) pairs tried by calibrate(): the roofline rule of the north
-    # star, the latency-balanced rule (R16b), each with unbounded and bounded claim-ahead
-    KNOBS = ((0, 0), (1, 0), (1, 2), (1, 3), (0, 3))
+    # the roofline rule of the north star, the latency-balanced rules (R16b), unbounded
+    # and bounded claim-ahead (R20), critical-path-first / round-robin / no stealing
+    # (partition rule, claim depth, steal mode) triples tried by calibrate()
+    KNOBS = ((0, 0, 2), (1, 0, 2), (1, 2, 2), (1, 3, 2), (0, 3, 2), (1, 3, 0), (1, 0, 1), (2, 2, 2))
 
     def calibrate(self, knobs=KNOBS, runs=7, rho=None):
         """Runtime-aware choice of the executor's scheduling knobs for this mix: the SM-partition
-        rule (MT_OPT_PARTITION) and the claim-ahead depth (MT_OPT_CLAIM_DEPTH).  Times the given
-        schedule (default all-concurrent) under each (rule, depth) pair and keeps the fastest
+        rule (MT_OPT_PARTITION), the claim-ahead depth (MT_OPT_CLAIM_DEPTH) and the stealing mode
+        (MT_OPT_STEAL).  Times the given schedule (default all-concurrent) under each triple and
+        keeps the fastest
         (median of `runs` device makespans) -- the paper's cost is measured latency (P:92-93,
         P:441); the knobs change which CTA runs a tile and when, never the outputs."""
-        from .mt import MT_OPT_CLAIM_DEPTH, MT_OPT_PARTITION
         if rho is None:
             rho = [[] for _ in self.graphs]
         self.ctx.set_schedule_pointers(rho)
         med = {}
         for k in knobs:
-            self.ctx.set_option(MT_OPT_PARTITION, k[0])
-            self.ctx.set_option(MT_OPT_CLAIM_DEPTH, k[1])
+            self.set_knobs(k)
             self.run()
             med[tuple(k)] = float(np.median([self.run()[0] for _ in range(runs)]))
         best = min(med, key=med.get)
@@ -78,9 +78,11 @@ class TenantMix:
         return best, med
 
     def set_knobs(self, knobs):
-        from .mt import MT_OPT_CLAIM_DEPTH, MT_OPT_PARTITION
+        """knobs = (partition rule, claim depth[, steal mode (default 2)])"""
+        from .mt import MT_OPT_CLAIM_DEPTH, MT_OPT_PARTITION, MT_OPT_STEAL
         self.ctx.set_option(MT_OPT_PARTITION, knobs[0])
         self.ctx.set_option(MT_OPT_CLAIM_DEPTH, knobs[1])
+        self.ctx.set_option(MT_OPT_STEAL, knobs[2] if len(knobs) > 2 else 2)
         self.knobs = tuple(knobs)
 
     def run(self, stream=0):

@@ -71,8 +71,8 @@ def main():
         r = {"tenants": list(configs.CONFIGS[cfg][0]), "ops": L}
         if not a.no_calibrate:   # executor knobs (partition rule, claim depth) chosen by measurement
             kn, med = m.calibrate()
-            r["knobs"] = {"sm_partition_rule": kn[0], "claim_depth": kn[1],
-                          "calibration_us": {f"{k[0]},{k[1]}": round(v, 1) for k, v in med.items()}}
+            r["knobs"] = {"sm_partition_rule": kn[0], "claim_depth": kn[1], "steal": kn[2] if len(kn) > 2 else 2,
+                          "calibration_us": {",".join(map(str, k)): round(v, 1) for k, v in med.items()}}
         for name, rho in (("all_concurrent", configs.all_concurrent_pointers(L)),
                           ("sequential_schedule", configs.sequential_pointers(L)),
                           ("uniform4", configs.uniform_pointers(L))):
@@ -110,7 +110,7 @@ def main():
 
 def render_md(res):
     """Markdown table of a zoo_table JSON (profiles/<round>_zoo_table.md body)."""
-    rows = ["| mix | knobs (rule, D) | all-conc. | rand | coord (P3,R2,M8) | seq sched. | SEQ | SEQ_G | MS_BFS | MS_G "
+    rows = ["| mix | knobs (rule, D, steal) | all-conc. | rand | coord (P3,R2,M8) | seq sched. | SEQ | SEQ_G | MS_BFS | MS_G "
             "| STAGE_EV | best vs SEQ_G | best vs MS_G | paper Seq / Stream / Ours-C |",
             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for cfg, r in res.items():
@@ -119,7 +119,7 @@ def render_md(res):
         pc = r.get("paper_context")
         paper = f"{pc['cudnn_seq_ms']} / {pc['stream_parallel_ms']} / {pc['ours_c_ms']} ({pc['table']})" if pc else "-"
         rows.append(
-            f"| {cfg}: {'+'.join(r['tenants'])} | {(kn['sm_partition_rule'], kn['claim_depth']) if kn else '(0, 0)'} "
+            f"| {cfg}: {'+'.join(r['tenants'])} | {(kn['sm_partition_rule'], kn['claim_depth'], kn.get('steal', 2)) if kn else '(0, 0, 2)'} "
             f"| {r['all_concurrent']:.3f} | {r['random_search']['ms']:.3f} | {r['coordinate_descent']['ms']:.3f} "
             f"| {r['sequential_schedule']:.3f} | {b['seq']:.3f} | {b['seq_graph']:.3f} | {b['ms_bfs']:.3f} "
             f"| {b['ms_graph']:.3f} | {b['stage_events']:.3f} | {min(b['seq'], b['seq_graph']) / r['best_executor_ms']:.2f}x "
