@@ -386,7 +386,7 @@ static mt_status plan_graphs(mt_ctx *c) {
           } else if (bf16) {
             d.tk = TK_CONV_TC;
             d.M = g.batch * os.h * os.w;
-            d.bn = os.c <= 16 ? 16 : os.c <= 32 ? 32 : os.c <= 64 ? 64 : 128;   // refined below
+            d.bn = os.c <= 16 ? 16 : os.c <= 32 ? 32 : os.c <= 64 ? 64 : os.c <= 128 ? 128 : 256;   // refined below
             d.tiles_n = (int)cdiv(os.c, d.bn);
             // TMA mainloop: whole output rows per M tile; a K-block is one tap x 64 channels, loaded
             // as one 4-D box {64 ch, Wo*sw, R*sh, 1} with element strides {1, sw, sh, 1}
@@ -434,7 +434,7 @@ static mt_status plan_graphs(mt_ctx *c) {
             int best_bn = d.bn, splits = 1;
             {
               double best = 1e30;
-              const int bn_max = d.bn;
+              const int bn_max = d.tma == 1 ? d.bn : std::min(d.bn, 128);   // 256-wide N tiles: TMA path only
               const double a_kb = d.tma ? (double)d.a_bytes : 16384.0;   // bytes of A per k-block
               const double rows = d.tma ? (double)d.blk_rows * d.seg_w : 128.0;
               for (int bn = bn_max; bn >= 32 || bn == bn_max; bn >>= 1) {

@@ -26,7 +26,7 @@ typedef __nv_bfloat16 bf16;
 // shared-memory map of a CTA (1024-aligned base)
 // ------------------------------------------------------------------------------------------
 static constexpr int PIPE_BYTES = MT_PIPE_BYTES;   // conv pipeline ring (stage geometry per op)
-static constexpr int TMEM_COLS = 128;
+static constexpr int TMEM_COLS = 256;   // accumulator of one 128 x 256 tile
 
 struct CtaShared {
   unsigned long long bar_full[MT_MAXST];     // TMA: stage loaded (expect_tx)
@@ -41,7 +41,7 @@ struct CtaShared {
   int cur[MT_MAXT], end[MT_MAXT], beg[MT_MAXT];
   uint32_t complete[64];      // bitset of ops observed fully complete (global op id < 2048)
   int16_t gate[MT_GATE_OPS];  // claim-ahead gate op of each op (-1 none; claim_depth != 0)
-  float esc[128], esh[128];   // epilogue scale / shift of the current conv tile's columns
+  float esc[256], esh[256];   // epilogue scale / shift of the current conv tile's columns
   OpDesc d;
 };
 static constexpr int SMEM_BYTES = 1024 + PIPE_BYTES;   // + static __shared__ CtaShared

@@ -278,3 +278,26 @@ def test_operand_path_edge_cases():
     errs = teacher_forced_errors(m, x, 0)
     assert max(errs) <= 1e-2, errs
     assert rel_err(m.outputs_numpy()[0], fw.forward(g, x, "bf16")) <= 1e-2
+
+
+def test_wide_n_tiles_bn256():
+    """128 x 256 accumulator tiles (TMA path, 256 TMEM columns, 4-stage ring): ragged second N tile
+    (Co = 320), fused residual, then a stride-2 conv; per-op teacher-forced vs the oracle at b=8"""
+    from paper_2111_14255_b200.session import TenantMix
+    b = zoo.GraphBuilder("tinyA", 8, 64, 28, 28, zoo.PREC_BF16, seed=7)
+    x0 = b.relu(-1)
+    x1 = b.conv(x0, 320, 3, 1, 1)
+    x2 = b.conv(x1, 320, 1, 1, 0, residual=x1)
+    x3 = b.conv(x2, 512, 3, 2, 1)
+    b.fc(b.gap(x3), 10)
+    g = b.build()
+    m = TenantMix([g])
+    plans = [m.ctx.op_plan(0, j) for j in range(g.n_ops)]
+    assert plans[1]["bn"] == 256 and plans[2]["bn"] == 256 and plans[1]["tiles_n"] == 2
+    x = zoo.make_input(g, seed=8)
+    m.set_input(x)
+    m.ctx.set_schedule_pointers([[]])
+    m.run()
+    errs = teacher_forced_errors(m, x, 0)
+    assert max(errs) <= 1e-2, errs
+    assert rel_err(m.outputs_numpy()[0], fw.forward(g, x, "bf16")) <= 1e-2
