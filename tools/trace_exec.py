@@ -115,8 +115,28 @@ print(f"{'op':>4} {'name':46} {'tiles':>5} {'start':>7} {'end':>7} {'wait':>6} {
 for r in rows:
     print(f"{r['op']:4d} {r['name'][:46]:46} {r['tiles']:5d} {r['start']:7.1f} {r['end']:7.1f} {r['wait_mean']:6.2f} "
           f"{r['work_mean']:6.2f} {r['work_max']:6.2f} {r['mma_mean']:6.2f} {r['run_mean']:6.2f} {r['rel_mean']:6.2f}")
+# per-tenant SM occupancy (north star: "SM occupancy per tenant slice"): busy SM-us of the
+# tenant's tiles, how many of them ran on CTAs homed on another tenant (stealing), and the busy
+# fraction of the tenant's home CTAs over the makespan
+bounds = np.cumsum([0] + L)
+ten_of = np.searchsorted(bounds, (tr[:, 0] & 0xffffffff), side="right") - 1
+home = tr[:, 6]
+sms = m.ctx.sm_partition().tolist()
+occ = []
+for t in range(len(L)):
+    sel = ten_of == t
+    w = (tr[sel, 5] - tr[sel, 3]).sum() / 1e3
+    stolen = int((home[sel] != t).sum())
+    hsel = home == t
+    hb = (tr[hsel, 5] - tr[hsel, 3]).sum() / 1e3
+    n_home = sms[0][t] if len(sms) == 1 else None
+    occ.append(dict(tenant=g[t].name, tiles=int(sel.sum()), busy_sm_us=round(float(w), 1), stolen_tiles=stolen,
+                    home_ctas=n_home,
+                    home_busy_frac=round(float(hb / (n_home * total)), 3) if n_home else None))
+    print(f"tenant {g[t].name:14s} tiles {int(sel.sum()):5d} busy {w:8.1f} SM-us  run by other tenants' CTAs {stolen:5d}"
+          + (f"  home CTAs {n_home:3d} busy {hb / (n_home * total):.3f} of makespan" if n_home else ""))
 busy = ((tr[:, 5] - tr[:, 3]).sum() / 1e3)
 print(f"SM-busy (work) us summed over CTAs: {busy:.1f}; makespan x CTAs: {total * 148:.1f} -> util {busy / (total * 148):.3f}")
 if a.out:
-    json.dump(dict(total=total, stages=stages, rows=rows), open(a.out, "w"), indent=1)
+    json.dump(dict(total=total, stages=stages, rows=rows, occupancy=occ), open(a.out, "w"), indent=1)
     np.save(a.out.replace(".json", "_raw.npy"), tr)
