@@ -300,7 +300,9 @@ def main():
         pmix.ctx.profile_batch_pointers(allc[:8], pmix.in_ptrs, pmix.out_ptrs, 1, 1, sp)  # warm
         barrier()
         t0 = time.perf_counter()
-        lat_all, st_all = D.profile_distributed(pfn, allc, rank, ws, device=dev)
+        pinfo = {}   # N > 1: every rank also times the two extremes (candidates 0, 1) for per-GPU scaling
+        lat_all, st_all = D.profile_distributed(pfn, allc, rank, ws, device=dev,
+                                                ref=(0, 1) if ws > 1 else None, info=pinfo)
         torch.cuda.synchronize(dev)
         dt = maxall(time.perf_counter() - t0)
         lat_p = lat_all[st_all == 0]
@@ -322,6 +324,7 @@ def main():
                      "best_us": float(np.nanmin(lat_p)) if len(lat_p) else None,
                      "median_us": float(np.nanmedian(lat_p)) if len(lat_p) else None,
                      "gather": "NCCL all_gather of per-rank latencies" if ws > 1 else "none (1 GPU)",
+                     "rank_scales": pinfo.get("scales"),
                      "search": search_line}
 
     cpu = None

@@ -64,3 +64,43 @@ def test_shard_indices_partition():
         for w in (1, 2, 3, 8):
             allc = sorted(c for r in range(w) for c in D.shard_indices(n, r, w))
             assert allc == list(range(n))
+
+
+def _slow_profile(rank):
+    """rank r's GPU runs 10 % * r slower than rank 0's"""
+    def f(cands):
+        lat, st = _fake_profile(cands)
+        return lat * (1.0 + 0.1 * rank), st
+    return f
+
+
+def _worker_norm(rank, world, port, n, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2111_14255_b200 import distributed as D
+    cands = configs.sample_candidates([56, 21, 54], n, seed=14255)
+    info = {}
+    lat, st = D.profile_distributed(_slow_profile(rank), cands, rank, world, ref=(0, 1), info=info)
+    out[rank] = (lat.tolist(), st.tolist(), info["scales"])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_profile_per_gpu_normalisation_gloo_world2():
+    """ranks with different clocks (rank 1 10 % slower): after scaling by the shared reference
+    schedules (the two extremes), every candidate's latency equals the average-GPU latency, so
+    candidates measured on different ranks are comparable (SURVEY §7 hard part 5)"""
+    pytest.importorskip("paper_2111_14255_b200.mt")
+    n = 40
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_worker_norm, args=(2, port, n, out), nprocs=2, join=True)
+        res = dict(out)
+    ref_lat, ref_st = _fake_profile(configs.sample_candidates([56, 21, 54], n, seed=14255))
+    for r in (0, 1):
+        lat, st, scales = res[r]
+        np.testing.assert_allclose(scales, [1.05, 1.05 / 1.1], rtol=1e-6)
+        np.testing.assert_allclose(np.array(lat), ref_lat * 1.05, rtol=1e-5)
+        np.testing.assert_array_equal(np.array(st, np.int32), ref_st)
