@@ -20,6 +20,15 @@ using namespace mt;
 
 static const int64_t BW_GBS = 8000;        // spec HBM GB/s (north star "8 TB/s")
 static const int64_t TC_GFLOPS = 2250000;  // spec dense bf16 GFLOP/s (2.25 PFLOP/s)
+// per-SM TMA operand bandwidth of the conv cost model, bytes per microsecond (traced: ~40-60 B/ns
+// per SM for the 4-D im2col boxes, tools/kb_rate.py); MT_TMA_BPUS overrides (tuning experiments)
+static double tma_bpus() {
+  static const double v = [] {
+    const char *e = getenv("MT_TMA_BPUS");
+    return e ? atof(e) : 160000.0;
+  }();
+  return v;
+}
 static const int64_t MT_HOP_NS = 2000;     // partition mode 2: dependency hop between ops (traces)
 
 struct mt_ctx {
@@ -439,7 +448,7 @@ static mt_status plan_graphs(mt_ctx *c) {
               const double rows = d.tma ? (double)d.blk_rows * d.seg_w : 128.0;
               for (int bn = bn_max; bn >= 32 || bn == bn_max; bn >>= 1) {
                 const int64_t tn = cdiv(os.c, bn), tmn_c = (int64_t)d.tiles_m * tn;
-                const double t_kb = std::max(0.13 * bn / 128.0, (a_kb + bn * 128.0) / 160000.0);
+                const double t_kb = std::max(0.13 * bn / 128.0, (a_kb + bn * 128.0) / tma_bpus());
                 for (int sp = 1; sp <= 12; ++sp) {
                   if (sp > 1 && d.nkb / sp < 2) break;
                   const int64_t kbps = cdiv(d.nkb, sp);
@@ -600,7 +609,7 @@ static mt_status plan_graphs(mt_ctx *c) {
     if (d.tk == TK_CONV_TC) {
       const double a_kb = d.tma ? (double)d.a_bytes : 16384.0;
       const double rows = d.tma == 3 ? 128.0 : d.tma ? (double)d.blk_rows * d.seg_w : 128.0;
-      const double t_kb = std::max(0.13 * d.bn / 128.0, (a_kb + d.bn * 128.0) / 160000.0);
+      const double t_kb = std::max(0.13 * d.bn / 128.0, (a_kb + d.bn * 128.0) / tma_bpus());
       const int64_t tmn = (int64_t)d.tiles_m * d.tiles_n;
       t0 = tmn * d.splits;
       us0 = 1.3 + d.kb_per_split * t_kb + (d.splits == 1 ? 1.3 + 0.01 * d.bn : 0.6);

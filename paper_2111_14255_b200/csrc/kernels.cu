@@ -35,6 +35,7 @@ struct CtaShared {
   uint32_t tmem_base;
   int op, tile, last, ok, home, ten;
   int smem_cap;               // bytes of dynamic shared memory this kernel has (staging budget)
+  int tracing;                // mt_set_trace on: extra producer stamps
   unsigned long long t_pick, t_pick_next, t_deps, t_mma, t_run, t_first, t_lastmma, t_aissue;
   unsigned long long t_kb[4], t_is[1];
   int *xrel;   // extra counter released with the tile (split-K partial arrival)
@@ -537,6 +538,10 @@ __device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const Conv
           }
         } else {
           tma_load_4d(st, tmap_a, bar, cb * 64, wbase + ss, hbase + rr, img);
+        }
+        if (sh.tracing && (i == 0 || i == nk - 1)) {   // producer issue stamps (trace only)
+          if (i == 0) sh.t_is[0] = gtimer();
+          if (i == nk - 1) sh.t_aissue = gtimer();
         }
       }
       __syncwarp();
@@ -1868,7 +1873,7 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
   __shared__ __align__(16) CtaShared sh;
   PipeState ps{0u, 0u, 0u};
   if (threadIdx.x < 64) sh.complete[threadIdx.x] = 0u;
-  if (threadIdx.x == 0) sh.smem_cap = PIPE_BYTES;
+  if (threadIdx.x == 0) { sh.smem_cap = PIPE_BYTES; sh.tracing = a.trace != nullptr; }
   if (a.claim_depth != 0)
     for (int i = threadIdx.x; i < a.n_ops; i += blockDim.x) sh.gate[i] = (int16_t)__ldg(a.gates + i);
   cta_setup(sh, true);
@@ -1910,7 +1915,7 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) op_kernel(RunArgs a, int op) {
   __shared__ __align__(16) CtaShared sh;
   PipeState ps{0u, 0u, 0u};
   load_desc(sh, a.ops + op);
-  if (threadIdx.x == 0) sh.smem_cap = PIPE_BYTES;
+  if (threadIdx.x == 0) { sh.smem_cap = PIPE_BYTES; sh.tracing = a.trace != nullptr; }
   const bool tc = __ldg(&a.ops[op].tk) == TK_CONV_TC;
   cta_setup(sh, tc);
   for (int t = blockIdx.x; t < sh.d.tiles; t += gridDim.x) {
@@ -1937,7 +1942,7 @@ __global__ void __launch_bounds__(MT_NTHREADS) op_kernel_small(RunArgs a, int op
   __shared__ __align__(16) CtaShared sh;
   PipeState ps{0u, 0u, 0u};
   load_desc(sh, a.ops + op);
-  if (threadIdx.x == 0) { sh.smem_cap = SMALL_SMEM - 1024; sh.xrel = nullptr; }
+  if (threadIdx.x == 0) { sh.smem_cap = SMALL_SMEM - 1024; sh.xrel = nullptr; sh.tracing = a.trace != nullptr; }
   __syncthreads();
   for (int t = blockIdx.x; t < sh.d.tiles; t += gridDim.x) {
     if (threadIdx.x == 0) { sh.t_pick = gtimer(); sh.t_mma = 0; sh.home = -1; }
