@@ -131,13 +131,39 @@ def oracle_sample(config, budget_s=10.0, max_reps=5):
     return float(np.mean(times)) * 1e3, len(times), cores
 
 
-def run_reference(args, ws, rank):
+def run_reference(args, ws, rank, budget_s=240.0):
+    """The tier's reference arm: the CPU oracle as it stands, on the host cores.  W untimed steps,
+    then K timed steps; a step = one full multi-tenant forward pass of the workload (all tenants,
+    one batch).  If K steps would exceed budget_s the run stops early and says so (steps = done)."""
     if rank != 0:
         return
+    from oracle import forward as fw
     cfg = args.config
-    ms, reps, cores = oracle_sample(cfg, budget_s=max(10.0, 0.0))
+    graphs = configs.tenants(cfg)
+    x = zoo.make_input(graphs[0])
+
+    def step():
+        for g in graphs:
+            fw.forward(g, x, "bf16")
+
+    for _ in range(args.warmup):
+        step()
+    times = []
+    t0 = time.perf_counter()
+    while len(times) < args.steps:
+        t1 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t1)
+        if time.perf_counter() - t0 + times[-1] > budget_s:
+            break
+    ms, reps = float(np.mean(times)) * 1e3, len(times)
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:
+        cores = os.cpu_count()
     line = {"impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus,
-            "steps": reps, "warmup": 0, "ms_per_step": ms, "higher_is_better": False,
+            "steps": reps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg} ({CONFIG_NAMES.get(cfg, cfg)}): " + configs.CONFIGS[cfg][3],
                        "parallelism": "cpu"},

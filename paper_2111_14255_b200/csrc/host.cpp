@@ -643,10 +643,10 @@ static mt_status plan_graphs(mt_ctx *c) {
   L.ctl = take(sizeof(CtlBlock));
   L.claim = take(sizeof(int32_t) * total);
   L.done = take(sizeof(int32_t) * total);
-  L.gates = take(sizeof(int32_t) * total);
   L.blk = take(sizeof(int32_t) * std::max(c->total_blocks, 1));
   L.splitcnt = take(sizeof(int32_t) * std::max(split_cnt, 1));
   L.counters_bytes = off;
+  L.gates = take(sizeof(int32_t) * total);   // outside the counters: error recovery zeroes those
   L.ops = take(sizeof(OpDesc) * total);
   L.tmaps = take((size_t)256 * total);
   L.sched_rng = take(sizeof(int32_t) * S_max * NT * 2);

@@ -1748,7 +1748,11 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
           }
           const int k = atomicAdd(a.claim + o, 1);
           if (k < __ldg(&a.ops[o].tiles)) { op = o; tile = k; ten = t; break; }
-          sh.cur[t] = o + 1;  // every tile of o is claimed
+          // every tile of o is claimed: publish that and jump to the furthest frontier any CTA
+          // has seen for this tenant (one atomic instead of one failed claim per op when a CTA
+          // catches up on a tenant it has not served, e.g. when stealing or at the stage end)
+          const int g = atomicMax(&a.ctl->gcur[t], o + 1);
+          sh.cur[t] = max(o + 1, g);
         }
       }
       if (op < 0 && blocked) {   // work remains but none is claimable yet: retry shortly
@@ -1905,6 +1909,7 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
     }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_blk; i += gridDim.x * blockDim.x)
       a.blkcnt[i] = 0;
+    if (blockIdx.x == 0 && threadIdx.x < MT_MAXT) a.ctl->gcur[threadIdx.x] = 0;
   }
   cta_teardown(sh, true);
 }

@@ -80,6 +80,7 @@ struct CtlBlock {
   unsigned int error;        // nonzero: a spin timed out / invariant broken
   unsigned int trace_count;  // entries written to the trace buffer
   unsigned long long err_info;
+  int gcur[MT_MAXT];         // per tenant: every op below is fully claimed (monotonic hint; reset per run)
 };
 
 struct RunArgs {

@@ -22,8 +22,9 @@ def _line(args, timeout):
 
 
 def test_reference_arm_line():
-    d = _line(["--impl", "reference", "--steps", "1", "--warmup", "3"], 900)
+    d = _line(["--impl", "reference", "--steps", "2", "--warmup", "1"], 900)
     assert d["impl"] == "reference"
+    assert d["steps"] == 2 and d["warmup"] == 1          # K timed steps after W untimed ones
     for k in KEYS:
         assert k in d, k
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
