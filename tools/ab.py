@@ -16,6 +16,7 @@ ap.add_argument("--libs", required=True)
 ap.add_argument("--configs", default="c2")
 ap.add_argument("--rounds", type=int, default=3)
 ap.add_argument("--runs", type=int, default=20)
+ap.add_argument("--knobs", default="0,0", help="config=rule,depth;... or one rule,depth for all")
 a = ap.parse_args()
 libs = a.libs.split(",")
 res = {}
@@ -23,8 +24,10 @@ for r in range(a.rounds):
     for cfg in a.configs.split(","):
         for lib in (libs if r % 2 == 0 else libs[::-1]):
             env = dict(os.environ, MT_LIB_PATH=os.path.abspath(lib))
+            kn = dict(x.split("=") for x in a.knobs.split(";")) if "=" in a.knobs else {}
             out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "prof_exec.py"), "--config", cfg,
-                                  "--runs", str(a.runs)], capture_output=True, text=True, env=env, timeout=300).stdout
+                                  "--runs", str(a.runs), "--knobs", kn.get(cfg, a.knobs if not kn else "0,0")],
+                                 capture_output=True, text=True, env=env, timeout=300).stdout
             us = [float(m) for m in re.findall(r"run \d+: ([0-9.]+) us", out)][3:]
             res.setdefault((cfg, lib), []).extend(us)
 for cfg in a.configs.split(","):
