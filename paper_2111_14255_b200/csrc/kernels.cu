@@ -1464,14 +1464,20 @@ __device__ void pack_pixels(const RunArgs &a, int t, int64_t first, int64_t stri
 // ------------------------------------------------------------------------------------------
 // tile dispatch (shared by the executor and the per-op baseline kernels)
 // ------------------------------------------------------------------------------------------
+// F32 = false: the kernel instantiation for mixes whose tenants all store bf16 -- the fp32 tile
+// variants (config 1 only) are compiled out, which keeps the persistent kernel's code (and its
+// instruction-cache footprint) smaller
+template <bool F32>
 __device__ void run_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_t *smem, CtaShared &sh,
                          PipeState &ps) {
-  const bool f32 = d.prec == 1;
+  const bool f32 = F32 && d.prec == 1;
   switch (d.tk) {
     case TK_CONV_TC: conv_tc_tile(a, d, tile, smem, sh, ps); return;
     case TK_CONV_SIMT:
-      if (f32) conv_simt_tile<float>(a, d, tile, smem);
-      else conv_simt_tile<bf16>(a, d, tile, smem);
+      if constexpr (F32) {
+        if (f32) conv_simt_tile<float>(a, d, tile, smem);
+        else conv_simt_tile<bf16>(a, d, tile, smem);
+      }
       break;
     case TK_DW: if (f32) dw_tile<float>(a, d, tile, smem, sh.smem_cap); else dw_tile<bf16>(a, d, tile, smem, sh.smem_cap); break;
     case TK_POOL: if (f32) pool_tile<float>(a, d, tile); else pool_tile<bf16>(a, d, tile); break;
@@ -1695,6 +1701,7 @@ __device__ __forceinline__ void trace_tile(const RunArgs &a, const CtaShared &sh
 // dependency of a claimed tile is itself claimed by a running CTA and the wait always ends
 // (all CTAs co-resident).  While the dependencies finish, the tile's weights are already
 // streamed into shared memory / L2 (tile_prefetch).
+template <bool F32>
 __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh, PipeState &ps) {
   const int T = a.n_tenants;
   const int tid = threadIdx.x;
@@ -1855,7 +1862,7 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
     }
     __syncthreads();
     if (!sh.ok) { cp_async_wait<0>(); return false; }
-    run_tile(a, sh.d, my_tile, smem, sh, ps);
+    run_tile<F32>(a, sh.d, my_tile, smem, sh, ps);
     if (tid == 0) {   // publish: this tile's outputs are visible (release)
       sh.t_run = gtimer();
       const int b = tile_block(sh.d, my_tile, sh);
@@ -1872,6 +1879,7 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
   }
 }
 
+template <bool F32>
 __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
   uint8_t *smem = smem_base();
   __shared__ __align__(16) CtaShared sh;
@@ -1896,7 +1904,7 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
     if (ok && blockIdx.x == 0 && threadIdx.x == 0 && a.ts && a.ts_full) a.ts[2] = gtimer();
   }
   for (int s = 0; ok && s < a.n_stages; ++s) {
-    ok = run_stage(a, s, smem, sh, ps);
+    ok = run_stage<F32>(a, s, smem, sh, ps);
     if (ok) ok = grid_barrier(a, sh);
     if (ok && blockIdx.x == 0 && threadIdx.x == 0 && a.ts && a.ts_full) a.ts[3 + s] = gtimer();
   }
@@ -1915,6 +1923,7 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
 }
 
 // baseline: all tiles of one op, grid-strided
+template <bool F32>
 __global__ void __launch_bounds__(MT_NTHREADS, 1) op_kernel(RunArgs a, int op) {
   uint8_t *smem = smem_base();
   __shared__ __align__(16) CtaShared sh;
@@ -1928,7 +1937,7 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) op_kernel(RunArgs a, int op) {
     tile_prefetch(sh.d, t, smem, sh, ps);
     if (threadIdx.x == 0) sh.t_deps = gtimer();
     __syncthreads();
-    run_tile(a, sh.d, t, smem, sh, ps);
+    run_tile<F32>(a, sh.d, t, smem, sh, ps);
     if (threadIdx.x == 0 && sh.xrel) {   // split-K partial arrival (reduce tiles of this launch spin on it)
       fence_acq_rel_gpu();
       red_relaxed_add(sh.xrel, 1);
@@ -1941,6 +1950,7 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) op_kernel(RunArgs a, int op) {
 
 // small-smem variant for non-tensor-core ops so several op kernels can share an SM
 static constexpr int SMALL_SMEM = 47 * 1024;   // <= 48 KB: no opt-in needed; 46 KB usable after alignment
+template <bool F32>
 __global__ void __launch_bounds__(MT_NTHREADS) op_kernel_small(RunArgs a, int op) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -1954,7 +1964,7 @@ __global__ void __launch_bounds__(MT_NTHREADS) op_kernel_small(RunArgs a, int op
     tile_prefetch(sh.d, t, smem, sh, ps);
     if (threadIdx.x == 0) sh.t_deps = gtimer();
     __syncthreads();
-    run_tile(a, sh.d, t, smem, sh, ps);
+    run_tile<F32>(a, sh.d, t, smem, sh, ps);
     if (threadIdx.x == 0) trace_tile(a, sh, op, t);
   }
 }
@@ -2027,12 +2037,18 @@ size_t executor_smem_bytes() { return SMEM_BYTES; }
 static cudaError_t set_attrs() {
   static bool done = false;
   if (done) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(executor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaError_t e = cudaFuncSetAttribute(executor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(op_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  e = cudaFuncSetAttribute(executor_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(op_kernel_small, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM);
-  if (e != cudaSuccess) return e;
+  for (auto f : {op_kernel<true>, op_kernel<false>}) {
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+  }
+  for (auto f : {op_kernel_small<true>, op_kernel_small<false>}) {
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM);
+    if (e != cudaSuccess) return e;
+  }
   done = true;
   return cudaSuccess;
 }
@@ -2040,15 +2056,17 @@ static cudaError_t set_attrs() {
 cudaError_t executor_occupancy(int *bps) {
   cudaError_t e = set_attrs();
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, executor_kernel, MT_NTHREADS, SMEM_BYTES);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, executor_kernel<true>, MT_NTHREADS, SMEM_BYTES);
 }
 
 cudaError_t launch_executor(const RunArgs &a, int grid, cudaStream_t s) {
   cudaError_t e = set_attrs();
   if (e != cudaSuccess) return e;
   void *args[] = {(void *)&a};
-  return cudaLaunchCooperativeKernel((void *)executor_kernel, dim3(grid), dim3(MT_NTHREADS), args,
-                                     SMEM_BYTES, s);
+  bool f32 = false;
+  for (int t = 0; t < a.n_tenants; ++t) f32 |= a.in_prec[t] == 1;
+  return cudaLaunchCooperativeKernel(f32 ? (void *)executor_kernel<true> : (void *)executor_kernel<false>,
+                                     dim3(grid), dim3(MT_NTHREADS), args, SMEM_BYTES, s);
 }
 
 cudaError_t launch_op(const RunArgs &a, const OpDesc &d, int op, int max_grid, cudaStream_t s) {
@@ -2056,11 +2074,13 @@ cudaError_t launch_op(const RunArgs &a, const OpDesc &d, int op, int max_grid, c
   if (e != cudaSuccess) return e;
   if (d.tk == TK_CONV_TC) {
     const int grid = d.tiles < max_grid ? d.tiles : max_grid;
-    op_kernel<<<grid, MT_NTHREADS, SMEM_BYTES, s>>>(a, op);
+    if (d.prec == 1) op_kernel<true><<<grid, MT_NTHREADS, SMEM_BYTES, s>>>(a, op);
+    else op_kernel<false><<<grid, MT_NTHREADS, SMEM_BYTES, s>>>(a, op);
   } else {
     const int cap = 4 * max_grid;
     const int grid = d.tiles < cap ? d.tiles : cap;
-    op_kernel_small<<<grid, MT_NTHREADS, SMALL_SMEM, s>>>(a, op);
+    if (d.prec == 1) op_kernel_small<true><<<grid, MT_NTHREADS, SMALL_SMEM, s>>>(a, op);
+    else op_kernel_small<false><<<grid, MT_NTHREADS, SMALL_SMEM, s>>>(a, op);
   }
   return cudaGetLastError();
 }

@@ -16,7 +16,7 @@ import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rep = sys.argv[1]
-kernel = sys.argv[2] if len(sys.argv) > 2 and not sys.argv[2].startswith("--") else "_ZN3mtk15executor_kernelE7RunArgs"
+kernel = sys.argv[2] if len(sys.argv) > 2 and not sys.argv[2].startswith("--") else "_ZN3mtk15executor_kernelILb0EEEv7RunArgs"
 top = int(sys.argv[sys.argv.index("--top") + 1]) if "--top" in sys.argv else 40
 src_csv = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src_csv)))

@@ -135,6 +135,18 @@ for t in range(len(L)):
                     home_busy_frac=round(float(hb / (n_home * total)), 3) if n_home else None))
     print(f"tenant {g[t].name:14s} tiles {int(sel.sum()):5d} busy {w:8.1f} SM-us  run by other tenants' CTAs {stolen:5d}"
           + (f"  home CTAs {n_home:3d} busy {hb / (n_home * total):.3f} of makespan" if n_home else ""))
+# per-CTA time split: waiting for dependencies (claimed, not ready), working (deps -> released),
+# and between tiles (release -> next pick: claiming, retries of bounded claim-ahead, stage end)
+cta = tr[:, 1] >> 32
+wait_t = ((tr[:, 3] - tr[:, 2]).sum()) / 1e3
+gap_t = 0.0
+for c in np.unique(cta):
+    r = tr[cta == c]
+    r = r[np.argsort(r[:, 2])]
+    gap_t += ((r[1:, 2] - r[:-1, 5]).clip(min=0).sum()) / 1e3
+last_end = (tr[:, 5].max() - t0) / 1e3
+print(f"CTA time: dependency wait {wait_t:.0f} us, between tiles {gap_t:.0f} us (summed over CTAs); "
+      f"last release at {last_end:.1f} us of stage {stages[0] if stages else 0:.1f} us")
 busy = ((tr[:, 5] - tr[:, 3]).sum() / 1e3)
 print(f"SM-busy (work) us summed over CTAs: {busy:.1f}; makespan x CTAs: {total * 148:.1f} -> util {busy / (total * 148):.3f}")
 if a.out:
