@@ -366,6 +366,8 @@ def main():
         line = {
             "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": ws, "steps": K, "warmup": W,
             "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "latency_stats_ms": {"mean": float(np.mean(step_ms)), "median": float(np.median(step_ms)),
+                                 "p90": float(np.percentile(step_ms, 90)), "rank": rank},
             "dtype": "bf16", "data": "synthetic (seeded LeCun-normal weights, identity-BN, N(0,1) input)",
             "config": {"workload": f"{args.config} ({CONFIG_NAMES.get(args.config, args.config)}): "
                                    + configs.CONFIGS[args.config][3],
