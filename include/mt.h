@@ -125,11 +125,15 @@ typedef enum {
                            /*    E_t(n) = sum over the slice's work items ceil(tiles/n)*ns  */
                            /*    (mt_op_work); 2: work/span, E_t(n) = ceil(W_t/n) + S_t.    */
                            /*    Setting it re-plans the active schedule.                   */
-  MT_OPT_CLAIM_DEPTH = 6   /* 0 (default): a CTA may claim any tile of its tenant's slice     */
+  MT_OPT_CLAIM_DEPTH = 6,  /* 0 (default): a CTA may claim any tile of its tenant's slice     */
                            /* (claim-then-wait).  D > 0: a tile of op o is claimable only   */
                            /* once o's ancestors at DAG distance D are complete; D < 0: once */
                            /* op o-|D| of the same tenant is complete (bounded claim-ahead: */
                            /* CTAs blocked everywhere retry instead of parking on a tile)   */
+  MT_OPT_STAGE_SPLIT = 7   /* 1: mt_run / mt_run_async launch the executor once per stage (the */
+                           /* kernel boundary replaces the grid barrier) so a profiler       */
+                           /* attributes counters per stage; debug/profiling only (launch    */
+                           /* gaps between stages); 0 (default): one cooperative launch      */
 } mt_option;
 
 /* execution modes of mt_run_baseline: the same tile functions launched one kernel per op */

@@ -38,6 +38,7 @@ struct mt_ctx {
   int grid = 148;
   int steal = 2;
   int claim_depth = 0; // MT_OPT_CLAIM_DEPTH
+  int stage_split = 0; // MT_OPT_STAGE_SPLIT
   int partition = 0;   // MT_OPT_PARTITION: 0 roofline-proportional, 1 latency-balanced, 2 work/span
   int64_t timeout_ms = 2000;
   bool loaded = false, bound = false, has_sched = false;
@@ -655,7 +656,7 @@ static mt_status plan_graphs(mt_ctx *c) {
   L.prof_area = take(L.prof_area_bytes);
   L.prof_ts_bytes = 1u << 20;
   L.prof_ts = take(L.prof_ts_bytes);
-  L.run_ts = take(sizeof(unsigned long long) * (S_max + 4));
+  L.run_ts = take(sizeof(unsigned long long) * 4 * (S_max + 1));   // stage-split: 4 stamps per launch
   L.packed_off.resize(NT);
   L.stage_in_off.resize(NT);
   L.stage_out_off.resize(NT);
@@ -1019,6 +1020,10 @@ mt_status mt_set_option(mt_ctx *c, int32_t option, int64_t value) {
         return fail(c, MT_ERR_ARG, "claim depth needs <= 2048 ops in the mix");
       c->claim_depth = (int)value;
       return upload_gates(c);
+    case MT_OPT_STAGE_SPLIT:
+      if (value < 0 || value > 1) return fail(c, MT_ERR_ARG, "stage split must be 0 or 1");
+      c->stage_split = (int)value;
+      return MT_OK;
     case MT_OPT_PARTITION:
       if (value < 0 || value > 2) return fail(c, MT_ERR_ARG, "partition must be 0, 1 or 2");
       c->partition = (int)value;
@@ -1244,7 +1249,25 @@ mt_status mt_run_async(mt_ctx *c, const float *const *inputs, float *const *outp
   if (st != MT_OK) return st;
   if (!inputs || !outputs) return fail(c, MT_ERR_ARG, "null inputs/outputs");
   RunArgs a = base_args(c, inputs, outputs);
-  CK(mtk::launch_executor(a, c->grid, (cudaStream_t)stream));
+  if (!c->stage_split) {
+    CK(mtk::launch_executor(a, c->grid, (cudaStream_t)stream));
+    return MT_OK;
+  }
+  // debug/profiling mode (SURVEY d.5): one launch per stage -- the kernel boundary is the stage
+  // barrier, so ncu attributes counters to stages; launch k stamps ts[4k .. 4k+3]
+  const int S = c->sched.S, N = (int)c->T.size();
+  unsigned long long *ts = (unsigned long long *)(c->ws + c->lay.run_ts);
+  for (int k = 0; k < S; ++k) {
+    RunArgs b = a;
+    b.rng = a.rng + (size_t)k * N * 2;
+    b.home = a.home + (size_t)k * c->grid;
+    b.n_stages = 1;
+    if (k > 0) b.n_pack = 0;
+    b.no_reset = k < S - 1;
+    b.ts = ts + 4 * k;
+    b.ts_full = 1;
+    CK(mtk::launch_executor(b, c->grid, (cudaStream_t)stream));
+  }
   return MT_OK;
 }
 
@@ -1253,12 +1276,18 @@ mt_status mt_run(mt_ctx *c, const float *const *inputs, float *const *outputs, f
   mt_status st = mt_run_async(c, inputs, outputs, stream);
   if (st != MT_OK) return st;
   const int S = c->sched.S;
-  std::vector<unsigned long long> ts(S + 3);
+  std::vector<unsigned long long> ts(c->stage_split ? 4 * S : S + 3);
   CK(cudaMemcpyAsync(ts.data(), c->ws + c->lay.run_ts, ts.size() * 8, cudaMemcpyDeviceToHost,
                      (cudaStream_t)stream));
   CK(cudaStreamSynchronize((cudaStream_t)stream));
   st = check_device_error(c);
   if (st != MT_OK) return st;
+  if (c->stage_split) {   // per launch k: [0] start, [1] end, [2] after the pack, [3] stage end
+    if (total_us) *total_us = (float)((double)(ts[4 * (S - 1) + 1] - ts[0]) * 1e-3);
+    if (stage_us)
+      for (int k = 0; k < S; ++k) stage_us[k] = (float)((double)(ts[4 * k + 3] - ts[4 * k + 2]) * 1e-3);
+    return MT_OK;
+  }
   if (total_us) *total_us = (float)((double)(ts[1] - ts[0]) * 1e-3);
   if (stage_us)
     for (int k = 0; k < S; ++k) stage_us[k] = (float)((double)(ts[3 + k] - ts[2 + k]) * 1e-3);

@@ -1911,6 +1911,8 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
   }
   if (ok) {
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.ts) a.ts[1] = gtimer();
+  }
+  if (ok && !a.no_reset) {
     // all tiles of the run are complete: reset the claim / done counters for the next launch
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ops; i += gridDim.x * blockDim.x) {
       a.claim[i] = 0;

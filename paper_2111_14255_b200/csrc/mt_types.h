@@ -98,6 +98,7 @@ struct RunArgs {
   unsigned long long *ts;    // [n_stages + 2] %globaltimer stamps (or NULL)
   unsigned long long timeout_ns;
   int32_t n_ops, ts_full;
+  int32_t no_reset;           // stage-split launches before the last: keep claim/done/block counters
   int32_t n_blk, trace_cap;
   unsigned long long *trace; // [trace_cap][8] per-tile records (debug; NULL = off)     // ts_full: 1 = all stage stamps, 0 = start/end only
   const float *inputs[MT_MAXT];     // per tenant user input (NCHW fp32)

@@ -244,9 +244,12 @@ def test_scheduling_knob_options_validated():
     c.set_option(mt.MT_OPT_PARTITION, 1)
     p1 = c.sm_partition().tolist()
     assert p0 != p1 and sum(p1[0]) == 148
-    for opt, bad in ((mt.MT_OPT_PARTITION, 3), (mt.MT_OPT_PARTITION, -1), (mt.MT_OPT_CLAIM_DEPTH, 1 << 21)):
+    for opt, bad in ((mt.MT_OPT_PARTITION, 3), (mt.MT_OPT_PARTITION, -1), (mt.MT_OPT_CLAIM_DEPTH, 1 << 21),
+                     (mt.MT_OPT_STAGE_SPLIT, 2)):
         with pytest.raises(Exception):
             c.set_option(opt, bad)
     assert c.sm_partition().tolist() == p1
     for d in (0, 1, 3, 100, -3):
         c.set_option(mt.MT_OPT_CLAIM_DEPTH, d)
+    c.set_option(mt.MT_OPT_STAGE_SPLIT, 1)
+    c.set_option(mt.MT_OPT_STAGE_SPLIT, 0)

@@ -301,3 +301,29 @@ def test_wide_n_tiles_bn256():
     errs = teacher_forced_errors(m, x, 0)
     assert max(errs) <= 1e-2, errs
     assert rel_err(m.outputs_numpy()[0], fw.forward(g, x, "bf16")) <= 1e-2
+
+
+def test_stage_split_launches_same_outputs():
+    """MT_OPT_STAGE_SPLIT (one launch per stage, SURVEY d.5 profiling mode): identical outputs to
+    the single cooperative launch, one stage time per stage, and the counters of the earlier
+    launches survive into the later ones (a later stage's ops depend on them)"""
+    from paper_2111_14255_b200 import mt as M
+    m = mix_for("c3")
+    L = [g.n_ops for g in m.graphs]
+    m.ctx.set_schedule_pointers(configs.uniform_pointers(L))
+    m.run()
+    ref = _outs(m)
+    m.ctx.set_option(M.MT_OPT_STAGE_SPLIT, 1)
+    try:
+        for _ in range(2):
+            for o in m.outputs:
+                o.zero_()
+            total, stages = m.run()
+            for a, b in zip(_outs(m), ref):
+                assert torch.equal(a, b)
+            assert len(stages) == 4 and all(s > 0 for s in stages) and total >= sum(stages)
+    finally:
+        m.ctx.set_option(M.MT_OPT_STAGE_SPLIT, 0)
+    m.run()
+    for a, b in zip(_outs(m), ref):
+        assert torch.equal(a, b)

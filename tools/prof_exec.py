@@ -20,6 +20,7 @@ ap.add_argument("--runs", type=int, default=5)
 ap.add_argument("--baseline", default=None)
 ap.add_argument("--steal", type=int, default=2)
 ap.add_argument("--knobs", default="0,0", help="partition rule, claim depth (TenantMix.calibrate)")
+ap.add_argument("--stage-split", action="store_true", help="one executor launch per stage (ncu per stage)")
 a = ap.parse_args()
 g = configs.tenants(a.config)
 L = [x.n_ops for x in g]
@@ -29,6 +30,8 @@ rho = {"all_concurrent": configs.all_concurrent_pointers, "sequential": configs.
        "uniform4": configs.uniform_pointers}[a.schedule](L)
 m.ctx.set_schedule_pointers(rho)
 m.set_knobs(tuple(int(v) for v in a.knobs.split(",")))
+if a.stage_split:
+    m.ctx.set_option(7, 1)
 for i in range(a.runs):
     if a.baseline:
         us = m.ctx.run_baseline(a.baseline, m.in_ptrs, m.out_ptrs)
