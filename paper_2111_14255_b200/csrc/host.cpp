@@ -29,7 +29,16 @@ static double tma_bpus() {
   }();
   return v;
 }
-static const int64_t MT_HOP_NS = 2000;     // partition mode 2: dependency hop between ops (traces)
+static const int64_t MT_HOP_NS = 2000;
+// per extra N tile of an M block (consumers wait for all of them; A re-read per N tile), us;
+// MT_TILE_PEN overrides (tuning experiments)
+static double tile_pen() {
+  static const double v = [] {
+    const char *e = getenv("MT_TILE_PEN");
+    return e ? atof(e) : 0.0;
+  }();
+  return v;
+}     // partition mode 2: dependency hop between ops (traces)
 
 struct mt_ctx {
   int device = -1;
@@ -454,7 +463,8 @@ static mt_status plan_graphs(mt_ctx *c) {
                   if (sp > 1 && d.nkb / sp < 2) break;
                   const int64_t kbps = cdiv(d.nkb, sp);
                   const int64_t waves = cdiv(tmn_c * sp, sm_avail);
-                  double t = waves * (1.3 + kbps * t_kb + (sp == 1 ? 1.3 + 0.01 * bn : 0.6));
+                  double t = waves * (1.3 + kbps * t_kb + (sp == 1 ? 1.3 + 0.01 * bn : 0.6)) +
+                             tile_pen() * (double)(tn - 1);
                   if (sp > 1) {
                     const int rcn = std::max(1, bn / 32);
                     t += 4.0 + cdiv(tmn_c * rcn, sm_avail) * (sp * rows * 32 * 4 / 50000.0);
