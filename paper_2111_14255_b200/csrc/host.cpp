@@ -206,7 +206,9 @@ static mt_status load_tenant(mt_ctx *c, int t, std::vector<std::vector<int>> &gr
 
 static mt_status plan_graphs(mt_ctx *c) {
   const int NT = (int)c->T.size();
-  const int sm_avail = std::max(24, 148 / std::max(NT, 1));   // cost model: SMs per op (shape + mix only)
+  // cost model: SMs per op (shape + mix only); MT_SM_AVAIL_SCALE scales it (tuning experiments)
+  static const double avail_scale = getenv("MT_SM_AVAIL_SCALE") ? atof(getenv("MT_SM_AVAIL_SCALE")) : 1.0;
+  const int sm_avail = std::min(148, (int)(avail_scale * std::max(24, 148 / std::max(NT, 1))));
   int total = 0;
   for (auto &tn : c->T) { tn.op_base = total; total += tn.L; }
   c->sum_L = total;
