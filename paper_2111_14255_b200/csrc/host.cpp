@@ -458,7 +458,8 @@ static mt_status plan_graphs(mt_ctx *c) {
               const int bn_max = d.tma == 1 ? d.bn : std::min(d.bn, 128);   // 256-wide N tiles: TMA path only
               const double a_kb = d.tma ? (double)d.a_bytes : 16384.0;   // bytes of A per k-block
               const double rows = d.tma ? (double)d.blk_rows * d.seg_w : 128.0;
-              for (int bn = bn_max; bn >= 32 || bn == bn_max; bn >>= 1) {
+              const int bn_min = getenv("MT_BN_MIN") ? atoi(getenv("MT_BN_MIN")) : 32;
+              for (int bn = bn_max; bn >= bn_min || bn == bn_max; bn >>= 1) {
                 const int64_t tn = cdiv(os.c, bn), tmn_c = (int64_t)d.tiles_m * tn;
                 const double t_kb = std::max(0.13 * bn / 128.0, (a_kb + bn * 128.0) / tma_bpus());
                 for (int sp = 1; sp <= 12; ++sp) {
@@ -473,7 +474,7 @@ static mt_status plan_graphs(mt_ctx *c) {
                   }
                   if (t < best * 0.97) { best = t; best_bn = bn; splits = sp; }
                 }
-                if (bn <= 32) break;
+                if (bn <= bn_min) break;
               }
             }
             d.bn = best_bn;
