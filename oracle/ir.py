@@ -202,14 +202,7 @@ def op_cost(graph_nodes, j, batch, in_chw, elem_bytes):
     return F, B
 
 
-def sm_partition(weights, n_sms):
-    """Split n_sms CTAs over tenants for one stage, n_t proportional to weights w_t
-    (w_t = sum over the tenant's slice of max(F*BW, B*TC), i.e. the slice's roofline time
-    scaled by BW*TC), by largest remainder:
-        active A = {t : w_t is not None}; R = n_sms - |A|;
-        n_t = 1 + floor(R*w_t/W) + [t among the (R - sum floor) largest remainders R*w_t mod W,
-              ties to the lower tenant index];   inactive tenants get 0.
-    If W == 0 every active tenant weighs 1."""
+def _largest_remainder(weights, n_sms):
     act = [t for t, w in enumerate(weights) if w is not None]
     out = [0] * len(weights)
     if not act:
@@ -228,6 +221,41 @@ def sm_partition(weights, n_sms):
         out[t] = 1 + base[t]
     for t in order[:left]:
         out[t] += 1
+    return out
+
+
+def sm_partition(weights, n_sms, caps=None):
+    """Split n_sms CTAs over tenants for one stage, n_t proportional to weights w_t
+    (w_t = sum over the tenant's slice of max(F*BW, B*TC), i.e. the slice's roofline time
+    scaled by BW*TC), by largest remainder:
+        active A = {t : w_t is not None}; R = n_sms - |A|;
+        n_t = 1 + floor(R*w_t/W) + [t among the (R - sum floor) largest remainders R*w_t mod W,
+              ties to the lower tenant index];   inactive tenants get 0.
+    If W == 0 every active tenant weighs 1.
+    SURVEY §8(a) a3 tile cap ("n_t <= the max tile count over the slice's ops; any excess is
+    redistributed"), caps[t] = that tile count: split over the free tenants U (initially A);
+    every tenant of U whose share exceeds its cap is fixed at the cap and leaves U; split the
+    SMs left over the new U; repeat.  When every tenant of U exceeds its cap the split over U
+    stands (the caps cannot absorb the GPU; reading R16)."""
+    out = _largest_remainder(weights, n_sms)
+    if caps is None:
+        return out
+    free = [w is not None for w in weights]
+    budget = n_sms
+    while True:
+        part = _largest_remainder([w if f else None for w, f in zip(weights, free)], budget)
+        U = [t for t in range(len(weights)) if free[t]]
+        if not U:
+            break
+        over = [t for t in U if part[t] > caps[t]]
+        if not over or len(over) == len(U):
+            for t in U:
+                out[t] = part[t]
+            break
+        for t in over:
+            out[t] = caps[t]
+            budget -= caps[t]
+            free[t] = False
     return out
 
 

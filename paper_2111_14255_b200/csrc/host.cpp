@@ -20,25 +20,12 @@ using namespace mt;
 
 static const int64_t BW_GBS = 8000;        // spec HBM GB/s (north star "8 TB/s")
 static const int64_t TC_GFLOPS = 2250000;  // spec dense bf16 GFLOP/s (2.25 PFLOP/s)
-// per-SM TMA operand bandwidth of the conv cost model, bytes per microsecond (traced: ~40-60 B/ns
-// per SM for the 4-D im2col boxes, tools/kb_rate.py); MT_TMA_BPUS overrides (tuning experiments)
-static double tma_bpus() {
-  static const double v = [] {
-    const char *e = getenv("MT_TMA_BPUS");
-    return e ? atof(e) : 160000.0;
-  }();
-  return v;
-}
-static const int64_t MT_HOP_NS = 2000;
-// per extra N tile of an M block (consumers wait for all of them; A re-read per N tile), us;
-// MT_TILE_PEN overrides (tuning experiments)
-static double tile_pen() {
-  static const double v = [] {
-    const char *e = getenv("MT_TILE_PEN");
-    return e ? atof(e) : 0.0;
-  }();
-  return v;
-}     // partition mode 2: dependency hop between ops (traces)
+// per-SM TMA operand bandwidth of the conv cost model, bytes per microsecond (calibrated on
+// executor traces, tools/kb_rate.py).  Plans depend only on the op's shape
+// and the mix's tenant count -- no environment input.
+static constexpr double TMA_BPUS = 160000.0;
+static const int64_t MT_HOP_NS = 2000;   // partition mode 2: dependency hop between ops (traces)
+static constexpr int BN_MIN = 32;        // narrowest N tile the cost model considers
 
 struct mt_ctx {
   int device = -1;
@@ -74,6 +61,13 @@ struct mt_ctx {
   int64_t trace_cap = 0;
   float *g_out[8][MT_MAXT] = {};
 };
+
+// cached baseline graphs capture RunArgs (workspace, trace buffer, timeout): drop them whenever
+// one of those changes
+static void drop_graphs(mt_ctx *c) {
+  for (auto &g : c->gexec)
+    if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+}
 
 static mt_status fail(mt_ctx *c, mt_status st, const std::string &msg) {
   if (c) {
@@ -206,9 +200,8 @@ static mt_status load_tenant(mt_ctx *c, int t, std::vector<std::vector<int>> &gr
 
 static mt_status plan_graphs(mt_ctx *c) {
   const int NT = (int)c->T.size();
-  // cost model: SMs per op (shape + mix only); MT_SM_AVAIL_SCALE scales it (tuning experiments)
-  static const double avail_scale = getenv("MT_SM_AVAIL_SCALE") ? atof(getenv("MT_SM_AVAIL_SCALE")) : 1.0;
-  const int sm_avail = std::min(148, (int)(avail_scale * std::max(24, 148 / std::max(NT, 1))));
+  // cost model: SMs per op (shape + mix only)
+  const int sm_avail = std::min(148, std::max(24, 148 / std::max(NT, 1)));
   int total = 0;
   for (auto &tn : c->T) { tn.op_base = total; total += tn.L; }
   c->sum_L = total;
@@ -458,16 +451,15 @@ static mt_status plan_graphs(mt_ctx *c) {
               const int bn_max = d.tma == 1 ? d.bn : std::min(d.bn, 128);   // 256-wide N tiles: TMA path only
               const double a_kb = d.tma ? (double)d.a_bytes : 16384.0;   // bytes of A per k-block
               const double rows = d.tma ? (double)d.blk_rows * d.seg_w : 128.0;
-              const int bn_min = getenv("MT_BN_MIN") ? atoi(getenv("MT_BN_MIN")) : 32;
+              const int bn_min = BN_MIN;
               for (int bn = bn_max; bn >= bn_min || bn == bn_max; bn >>= 1) {
                 const int64_t tn = cdiv(os.c, bn), tmn_c = (int64_t)d.tiles_m * tn;
-                const double t_kb = std::max(0.13 * bn / 128.0, (a_kb + bn * 128.0) / tma_bpus());
+                const double t_kb = std::max(0.13 * bn / 128.0, (a_kb + bn * 128.0) / TMA_BPUS);
                 for (int sp = 1; sp <= 12; ++sp) {
                   if (sp > 1 && d.nkb / sp < 2) break;
                   const int64_t kbps = cdiv(d.nkb, sp);
                   const int64_t waves = cdiv(tmn_c * sp, sm_avail);
-                  double t = waves * (1.3 + kbps * t_kb + (sp == 1 ? 1.3 + 0.01 * bn : 0.6)) +
-                             tile_pen() * (double)(tn - 1);
+                  double t = waves * (1.3 + kbps * t_kb + (sp == 1 ? 1.3 + 0.01 * bn : 0.6));
                   if (sp > 1) {
                     const int rcn = std::max(1, bn / 32);
                     t += 4.0 + cdiv(tmn_c * rcn, sm_avail) * (sp * rows * 32 * 4 / 50000.0);
@@ -623,7 +615,7 @@ static mt_status plan_graphs(mt_ctx *c) {
     if (d.tk == TK_CONV_TC) {
       const double a_kb = d.tma ? (double)d.a_bytes : 16384.0;
       const double rows = d.tma == 3 ? 128.0 : d.tma ? (double)d.blk_rows * d.seg_w : 128.0;
-      const double t_kb = std::max(0.13 * d.bn / 128.0, (a_kb + d.bn * 128.0) / tma_bpus());
+      const double t_kb = std::max(0.13 * d.bn / 128.0, (a_kb + d.bn * 128.0) / TMA_BPUS);
       const int64_t tmn = (int64_t)d.tiles_m * d.tiles_n;
       t0 = tmn * d.splits;
       us0 = 1.3 + d.kb_per_split * t_kb + (d.splits == 1 ? 1.3 + 0.01 * d.bn : 0.6);
@@ -742,6 +734,7 @@ static void build_stage_plan(mt_ctx *c, Schedule &s) {
   for (int k = 0; k < s.S; ++k) {
     std::vector<bool> active(N, false);
     std::vector<__int128> w(N, 0);
+    std::vector<int64_t> caps(N, 0);   // a3 tile cap: most tiles of one op of the slice
     for (int t = 0; t < N; ++t) {
       const int b = s.ranges[(k * N + t) * 2], e = s.ranges[(k * N + t) * 2 + 1];
       if (b == e) continue;
@@ -750,6 +743,7 @@ static void build_stage_plan(mt_ctx *c, Schedule &s) {
         const HostOp &h = c->ops[c->T[t].op_base + j];
         const __int128 a = (__int128)h.flops * BW_GBS, bb = (__int128)h.bytes * TC_GFLOPS;
         w[t] += a > bb ? a : bb;
+        caps[t] = std::max<int64_t>(caps[t], h.d.tiles);
       }
     }
     std::vector<int> n;
@@ -765,7 +759,7 @@ static void build_stage_plan(mt_ctx *c, Schedule &s) {
       }
       n = sm_partition_balanced(active, items, c->n_sms, c->partition, MT_HOP_NS);
     } else {
-      n = sm_partition(active, w, c->n_sms);
+      n = sm_partition(active, w, c->n_sms, &caps);
     }
     int cta = 0;
     for (int t = 0; t < N; ++t) {
@@ -1025,6 +1019,7 @@ mt_status mt_set_option(mt_ctx *c, int32_t option, int64_t value) {
     case MT_OPT_TIMEOUT_MS:
       if (value < 1) return fail(c, MT_ERR_ARG, "bad timeout");
       c->timeout_ms = value;
+      drop_graphs(c);
       return MT_OK;
     case MT_OPT_CTAS_PER_SM: return value == 1 ? MT_OK : fail(c, MT_ERR_ARG, "only 1 CTA/SM");
     case MT_OPT_CLAIM_DEPTH:
@@ -1054,9 +1049,8 @@ mt_status mt_load_graphs(mt_ctx *c, int32_t n, const mt_graph *graphs) {
   if (n < 1 || n > MT_MAX_TENANTS || !graphs) return fail(c, MT_ERR_ARG, "n_tenants out of range");
   if (n > c->n_sms) return fail(c, MT_ERR_ARG, "more tenants than SMs");
   if (!c->host_only) cudaDeviceSynchronize();
+  drop_graphs(c);
   c->loaded = c->bound = c->has_sched = false;
-  for (auto &g : c->gexec)
-    if (g) { cudaGraphExecDestroy(g); g = nullptr; }
   c->T.assign(n, Tenant{});
   for (int t = 0; t < n; ++t) {
     const mt_graph &g = graphs[t];
@@ -1148,6 +1142,7 @@ mt_status mt_bind_workspace(mt_ctx *c, void *dev, size_t bytes) {
   if (c->host_only) return fail(c, MT_ERR_STATE, "host-only context has no workspace");
   if (!c->loaded) return fail(c, MT_ERR_STATE, "no graphs loaded");
   if (!dev || bytes < c->lay.total || ((uintptr_t)dev & 255)) return fail(c, MT_ERR_ARG, "workspace too small or misaligned");
+  drop_graphs(c);
   c->ws = (char *)dev;
   c->ws_bytes = bytes;
   const Layout &L = c->lay;
@@ -1462,7 +1457,7 @@ mt_status mt_run_baseline(mt_ctx *c, int32_t mode, const float *const *inputs,
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
   if (total_us) *total_us = ms * 1000.f;
-  return MT_OK;
+  return check_device_error(c);   // a device timeout fails this call and is cleared here
 }
 
 // ---- profiling (a10) ---------------------------------------------------------------------
@@ -1633,6 +1628,7 @@ mt_status mt_set_trace(mt_ctx *c, void *dev, int64_t capacity) {
   mt_status st = check_ready(c, false);
   if (st != MT_OK) return st;
   if (capacity < 0 || capacity > (1 << 30) || (capacity > 0 && !dev)) return fail(c, MT_ERR_ARG, "bad trace buffer");
+  drop_graphs(c);
   c->trace = capacity > 0 ? (unsigned long long *)dev : nullptr;
   c->trace_cap = capacity;
   CK(cudaMemset(c->ws + c->lay.ctl + offsetof(CtlBlock, trace_count), 0, sizeof(unsigned)));

@@ -124,6 +124,12 @@ __device__ __forceinline__ void cp_async_wait() {
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// generic-proxy global writes (epilogue stores, input pack) of other CTAs, acquired through the
+// dependency counters, are read here by TMA (async proxy): order the acquire before the bulk
+// tensor loads (consumer side) and the stores before the release (producer side)
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
@@ -515,6 +521,7 @@ __device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const Conv
     const uint32_t eph = ps.eph;
     int s = 0, j = 0;
     uint32_t st = s0;
+    fence_proxy_async_global();   // dependencies acquired (generic proxy) -> TMA reads (async proxy)
     for (int i = 0; i < nk; ++i) {
       if (j > 0) mbar_wait(bar_empty0 + 8 * s, ((eph >> s) & 1u) ^ (uint32_t)((j - 1) & 1));
       if (elect_one()) {
@@ -1868,6 +1875,7 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
       sh.t_run = gtimer();
       const int b = tile_block(sh.d, my_tile, sh);
       const int boff = sh.d.blk_off;
+      fence_proxy_async_global();   // the tile's generic stores, before the release, for TMA readers
       fence_acq_rel_gpu();
       if (sh.xrel) { red_relaxed_add(sh.xrel, 1); sh.xrel = nullptr; }
       if (b >= 0) red_relaxed_add(a.blkcnt + boff + b, 1);
@@ -1901,6 +1909,7 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
       if (a.in_prec[t] == 1) pack_pixels<float>(a, t, first, stride);
       else pack_pixels<bf16>(a, t, first, stride);
     }
+    fence_proxy_async_global();   // packed input (generic stores) is read by the stems' TMA
     ok = grid_barrier(a, sh);
     if (ok && blockIdx.x == 0 && threadIdx.x == 0 && a.ts && a.ts_full) a.ts[2] = gtimer();
   }
@@ -1925,9 +1934,11 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
   cta_teardown(sh, true);
 }
 
-// baseline: all tiles of one op, grid-strided
+// baseline: tiles [t0, t1) of one op, grid-strided.  Split-K ops are issued as two launches
+// (partials, then the reduce tiles), so no tile of a non-cooperative launch waits on another
+// CTA of the same launch.
 template <bool F32>
-__global__ void __launch_bounds__(MT_NTHREADS, 1) op_kernel(RunArgs a, int op) {
+__global__ void __launch_bounds__(MT_NTHREADS, 1) op_kernel(RunArgs a, int op, int t0, int t1) {
   uint8_t *smem = smem_base();
   __shared__ __align__(16) CtaShared sh;
   PipeState ps{0u, 0u, 0u};
@@ -1935,13 +1946,13 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) op_kernel(RunArgs a, int op) {
   if (threadIdx.x == 0) { sh.smem_cap = PIPE_BYTES; sh.tracing = a.trace != nullptr; }
   const bool tc = __ldg(&a.ops[op].tk) == TK_CONV_TC;
   cta_setup(sh, tc);
-  for (int t = blockIdx.x; t < sh.d.tiles; t += gridDim.x) {
+  for (int t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
     if (threadIdx.x == 0) { sh.t_pick = gtimer(); sh.t_mma = 0; sh.home = -1; }
     tile_prefetch(sh.d, t, smem, sh, ps);
     if (threadIdx.x == 0) sh.t_deps = gtimer();
     __syncthreads();
     run_tile<F32>(a, sh.d, t, smem, sh, ps);
-    if (threadIdx.x == 0 && sh.xrel) {   // split-K partial arrival (reduce tiles of this launch spin on it)
+    if (threadIdx.x == 0 && sh.xrel) {   // split-K partial arrival (the reduce launch checks it)
       fence_acq_rel_gpu();
       red_relaxed_add(sh.xrel, 1);
       sh.xrel = nullptr;
@@ -2076,9 +2087,14 @@ cudaError_t launch_op(const RunArgs &a, const OpDesc &d, int op, int max_grid, c
   cudaError_t e = set_attrs();
   if (e != cudaSuccess) return e;
   if (d.tk == TK_CONV_TC) {
-    const int grid = d.tiles < max_grid ? d.tiles : max_grid;
-    if (d.prec == 1) op_kernel<true><<<grid, MT_NTHREADS, SMEM_BYTES, s>>>(a, op);
-    else op_kernel<false><<<grid, MT_NTHREADS, SMEM_BYTES, s>>>(a, op);
+    const int nc = d.splits > 1 ? d.tiles_m * d.tiles_n * d.splits : d.tiles;   // compute tiles
+    for (int part = 0; part < 2; ++part) {
+      const int t0 = part ? nc : 0, t1 = part ? d.tiles : nc;
+      if (t1 <= t0) continue;
+      const int grid = t1 - t0 < max_grid ? t1 - t0 : max_grid;
+      if (d.prec == 1) op_kernel<true><<<grid, MT_NTHREADS, SMEM_BYTES, s>>>(a, op, t0, t1);
+      else op_kernel<false><<<grid, MT_NTHREADS, SMEM_BYTES, s>>>(a, op, t0, t1);
+    }
   } else {
     const int cap = 4 * max_grid;
     const int grid = d.tiles < cap ? d.tiles : cap;

@@ -60,8 +60,8 @@ mt_error_info pointers_to_ranges(const std::vector<int> &L, int P, const int32_t
 
 // n_t proportional to w_t by largest remainder; every active tenant gets >= 1 CTA; ties in the
 // remainder go to the lower tenant index; inactive tenants get 0; all weights 0 -> equal.
-std::vector<int> sm_partition(const std::vector<bool> &active, const std::vector<__int128> &w,
-                              int n_sms) {
+static std::vector<int> lr_split(const std::vector<bool> &active, const std::vector<__int128> &w,
+                                 int n_sms) {
   const int N = (int)active.size();
   std::vector<int> out(N, 0);
   int A = 0;
@@ -93,6 +93,39 @@ std::vector<int> sm_partition(const std::vector<bool> &active, const std::vector
       if (rem[y] > rem[x] || (rem[y] == rem[x] && y < x)) { order[a] = y; order[b] = x; }
     }
   for (int k = 0; k < left && k < (int)order.size(); ++k) out[order[k]] += 1;
+  return out;
+}
+
+// SURVEY §8(a) a3 tile cap: n_t <= cap_t (the most tiles of one op of the slice: more CTAs cannot
+// run in parallel on the slice), the excess redistributed.  Water-filling: split over the free
+// tenants U (initially every active one) with lr_split; the tenants of U over their cap are fixed
+// at the cap and leave U; repeat with the SMs left.  If every tenant of U is over its cap the
+// last split stands (the GPU cannot be filled within the caps; the excess stays proportional).
+std::vector<int> sm_partition(const std::vector<bool> &active, const std::vector<__int128> &w,
+                              int n_sms, const std::vector<int64_t> *caps) {
+  std::vector<int> out = lr_split(active, w, n_sms);
+  if (!caps) return out;
+  const int N = (int)active.size();
+  std::vector<bool> U = active;
+  int budget = n_sms;
+  while (true) {
+    std::vector<int> part = lr_split(U, w, budget);
+    int nu = 0, nover = 0;
+    for (int t = 0; t < N; ++t)
+      if (U[t]) { ++nu; nover += part[t] > (*caps)[t]; }
+    if (nu == 0) break;
+    if (nover == 0 || nover == nu) {
+      for (int t = 0; t < N; ++t)
+        if (U[t]) out[t] = part[t];
+      break;
+    }
+    for (int t = 0; t < N; ++t)
+      if (U[t] && part[t] > (*caps)[t]) {
+        out[t] = (int)(*caps)[t];
+        budget -= out[t];
+        U[t] = false;
+      }
+  }
   return out;
 }
 

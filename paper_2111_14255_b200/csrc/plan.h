@@ -79,7 +79,8 @@ mt_error_info validate(const std::vector<int> &L, int S, const int32_t *ranges);
 mt_error_info pointers_to_ranges(const std::vector<int> &L, int P, const int32_t *rho,
                                  std::vector<int32_t> &ranges);
 std::vector<int> sm_partition(const std::vector<bool> &active,
-                              const std::vector<__int128> &w, int n_sms);
+                              const std::vector<__int128> &w, int n_sms,
+                              const std::vector<int64_t> *caps = nullptr);
 // latency-balanced partition: items[t] = (tiles, ns per tile) of each op of tenant t's slice
 std::vector<int> sm_partition_balanced(const std::vector<bool> &active,
                                        const std::vector<std::vector<std::pair<int64_t, int64_t>>> &items,

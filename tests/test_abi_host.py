@@ -168,7 +168,9 @@ def test_op_cost_and_sm_partition_match_oracle(config):
         c.set_schedule_pointers(rho)
         c.set_option(mt.MT_OPT_PARTITION, 0)      # roofline-proportional (north star)
         got = c.sm_partition().tolist()
-        exp = [ir.sm_partition(w, 148) for w in ir.stage_weights(graphs, ranges, eb_of)]
+        caps = [[max([c.op_tiles(t, j) for j in range(b, e)] or [0]) for t, (b, e) in enumerate(st)]
+                for st in ranges]   # a3 tile cap: most tiles of one op of the slice
+        exp = [ir.sm_partition(w, 148, cp) for w, cp in zip(ir.stage_weights(graphs, ranges, eb_of), caps)]
         assert got == exp
         for mode in (1, 2):                        # latency-balanced (R16b)
             c.set_option(mt.MT_OPT_PARTITION, mode)

@@ -77,6 +77,37 @@ def test_fc_and_gap_nodes_vs_torch():
                                rtol=1e-13)
 
 
+@pytest.mark.parametrize("act", [0, 1, 2])
+def test_standalone_bn_relu_add_nodes_vs_torch(act):
+    """The unfused BN / RELU / ADD operators (P:241 lists conv, bn, relu, pooling as the
+    operator kinds; SURVEY a1 keeps standalone nodes schedulable) against torch's own BN
+    (inference statistics), ReLU / ReLU6 and tensor sums."""
+    C = 8
+    x = RNG.standard_normal((2, C, 5, 6))
+    acts = {0: lambda t: t, 1: F.relu, 2: F.relu6}
+    # BN with running statistics, folded to (scale, shift) as the workload generator does
+    mu, var = RNG.standard_normal(C), RNG.uniform(0.5, 2.0, C)
+    gamma, beta, eps = RNG.uniform(0.5, 1.5, C), RNG.standard_normal(C), 1e-5
+    scale = (gamma / np.sqrt(var + eps)).astype(np.float32)
+    shift = (beta - mu * gamma / np.sqrt(var + eps)).astype(np.float32)
+    ref = acts[act](F.batch_norm(torch.tensor(x), torch.tensor(mu), torch.tensor(var),
+                                 torch.tensor(gamma), torch.tensor(beta), False, 0.0, eps)).numpy()
+    y = fw.eval_node(dict(kind=fw.BN, act=act), dict(scale=scale, shift=shift), [x], None)
+    np.testing.assert_allclose(y, ref, rtol=1e-6, atol=1e-6)   # fp32-rounded scale/shift
+    # RELU node: its act field selects ReLU (1) or ReLU6 (2); 0 is the identity
+    y = fw.eval_node(dict(kind=fw.RELU, act=act), {}, [x * 4], None)
+    np.testing.assert_array_equal(y, acts[act](torch.tensor(x * 4)).numpy())
+    # ADD of three inputs (+act): a sum, not a concat
+    xs = [RNG.standard_normal((2, C, 5, 6)) for _ in range(3)]
+    y = fw.eval_node(dict(kind=fw.ADD, act=act), {}, xs, None)
+    ref = acts[act](torch.tensor(xs[0]) + torch.tensor(xs[1]) + torch.tensor(xs[2])).numpy()
+    np.testing.assert_allclose(y, ref, rtol=1e-15, atol=1e-15)
+    # storage rounding: bf16 mode rounds the op output like torch's fp32 -> bf16 cast
+    yb = fw.eval_node(dict(kind=fw.ADD, act=act), {}, xs, None, mode="bf16")
+    exp = torch.tensor(ref).float().bfloat16().double().numpy()
+    np.testing.assert_array_equal(yb, exp)
+
+
 # --- whole models vs torchvision (same weights, fp64) --------------------------------------
 
 def _load_into_torchvision(graph, model):
@@ -123,6 +154,7 @@ TV = {
     "vgg16": lambda tv: tv.vgg16(),
     "alexnet": lambda tv: tv.alexnet(),
     "resnet34": lambda tv: tv.resnet34(),
+    "resnet101": lambda tv: tv.resnet101(),
 }
 
 

@@ -365,9 +365,10 @@ def squeezenet1_0(batch=1, precision=PREC_BF16):
     return b.build()
 
 
-def inception_v3(batch=1, precision=PREC_BF16):
-    """Inception-v3 at 224x224 (R19), no aux head, transform_input off."""
-    b = GraphBuilder("inception_v3", batch, 3, 224, 224, precision)
+def inception_v3(batch=1, precision=PREC_BF16, size=224):
+    """Inception-v3 at 224x224 (R15), no aux head, transform_input off.  `size` only
+    serves the oracle pin against torchvision's published cost at its native 299x299."""
+    b = GraphBuilder("inception_v3", batch, 3, size, size, precision)
     C = b.conv
     x = C(-1, 32, 3, 2, 0)
     x = C(x, 32, 3, 1, 0)
