@@ -91,6 +91,27 @@ def coordinate_descent(profile_fn, lengths, P: int, rounds: int, m: int, seed: i
     return res                                    # L14-15: global best of D
 
 
+def coordinate_descent_over_p(profile_fn, lengths, p_values, rounds: int, m: int,
+                              seed: int = 0) -> SearchResult:
+    """Alg.1 with the stage count searched too (R18b): Alg.1 fixes P (rho[N, P]),
+    so with a fixed P > 0 it can never return a schedule with fewer stages -- the all-concurrent
+    schedule (P = 0) in particular, whose matrix has no pointers at all.  For every P of p_values
+    (ascending) run Alg.1 (P = 0 is its single candidate); D collects every evaluation and the
+    global best of D is returned (L14-15).  Evaluations = sum over P of (1 + rounds * N * m) for
+    P > 0, 1 for P = 0."""
+    res = SearchResult(best_rho=None, best_lat=float("inf"))
+    for k, P in enumerate(p_values):
+        if P == 0:
+            rho = [[] for _ in lengths]
+            lat, st = profile_fn([rho])
+            _record(res, [rho], lat, st)
+            continue
+        r = coordinate_descent(profile_fn, lengths, P, rounds, m, seed=seed + k)
+        for rho, l, s in r.records:
+            _record(res, [rho], [l], [s])
+    return res
+
+
 def prefiltered_search(estimate_fn, profile_fn, candidates, keep: int) -> SearchResult:
     """rank `candidates` by the analytic estimate (estimate_fn(cands) -> (est,
     status), e.g. Context.estimate_batch_pointers; microseconds of host time per candidate), then

@@ -40,3 +40,26 @@ def test_our_arm_line_short():
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] == 5
     assert d["roofline"]["frac"] > 0 and d["roofline"]["peak"] > 0
     assert d["profiling"]["candidates"] == 16
+
+
+@pytest.mark.parametrize("config,sched,expect_us,tol", [
+    ("c2", "all_concurrent", 3.86, 0.02), ("c2", "uniform", 4.56, 0.02), ("c3", "all_concurrent", 41.9, 0.05),
+    ("c4", "all_concurrent", 48.3, 0.15), ("c4b8", "all_concurrent", 167.3, 0.1)])
+def test_stage_roofline_matches_survey_d4(config, sched, expect_us, tol):
+    """bench.py's per-stage roofline (max(F_s/TC, B_s/HBM), B_s = stage B_min) at the spec peaks
+    reproduces SURVEY §8(d) d.4's derived mix / per-schedule bounds"""
+    import numpy as np
+
+    import bench
+    from paper_2111_14255_b200 import mt
+    from workloads import configs, zoo
+    gs = configs.tenants(config)
+    L = [g.n_ops for g in gs]
+    c = mt.Context(-1)
+    c.load_graphs(gs, [[(0x1000, 0x2000, 0x3000) if g.params[j] else None for j in range(g.n_ops)] for g in gs])
+    c.set_schedule_pointers({"all_concurrent": configs.all_concurrent_pointers,
+                             "uniform": configs.uniform_pointers}[sched](L))
+    F, Wb = bench.op_tables(c, gs)
+    r = bench.stage_rooflines(np.asarray(c.get_schedule()).tolist(), gs, F, Wb, 2.25e15, 8e12,
+                              zoo.make_input(gs[0]).nbytes)
+    assert abs(sum(v[0] for v in r) * 1e6 - expect_us) <= tol

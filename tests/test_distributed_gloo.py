@@ -104,3 +104,49 @@ def test_sharded_profile_per_gpu_normalisation_gloo_world2():
         np.testing.assert_allclose(scales, [1.05, 1.05 / 1.1], rtol=1e-6)
         np.testing.assert_allclose(np.array(lat), ref_lat * 1.05, rtol=1e-5)
         np.testing.assert_array_equal(np.array(st, np.int32), ref_st)
+
+
+def _worker_bench(rank, world, port, n, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    L = [56, 21, 54]
+    cands = configs.sample_candidates(L, n, seed=14255)
+    res = bench.profiling_leg(_fake_profile, cands, L, rank, world, cd_p=(0, 1, 2), cd_m=4)
+    out[rank] = (res["lat"].tolist(), res["st"].tolist(), res["cd"]["best_us"], res["cd"]["evaluations"],
+                 res["cd"]["best_P"])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bench_profiling_leg_multirank_gloo_world2():
+    """bench.py's multi-rank profiling code path (sharded profiling + distributed coordinate
+    descent over P, one gather per (round, row)) with a stand-in profiler: every rank ends with
+    the 1-rank result, so the N-GPU bench line is the same computation spread over N GPUs"""
+    import bench
+    n = 48
+    L = [56, 21, 54]
+    one = bench.profiling_leg(_fake_profile, configs.sample_candidates(L, n, seed=14255), L, 0, 1,
+                              cd_p=(0, 1, 2), cd_m=4)
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_worker_bench, args=(2, port, n, out), nprocs=2, join=True)
+        res = dict(out)
+    for r in (0, 1):
+        lat, st, best, ev, bp = res[r]
+        np.testing.assert_array_equal(np.array(lat, np.float32), one["lat"])
+        np.testing.assert_array_equal(np.array(st, np.int32), one["st"])
+        assert best == one["cd"]["best_us"] and ev == one["cd"]["evaluations"] and bp == one["cd"]["best_P"]
+    assert one["cd"]["evaluations"] == 1 + 2 * (1 + 3 * 4)
+
+
+def test_bench_spawns_torchrun_for_multi_gpu():
+    """--gpus N > 1 without WORLD_SIZE re-launches bench.py under torch.distributed.run (the
+    driver's own launch line), so n_gpus reports the ranks"""
+    import bench
+    cmd = bench.torchrun_cmd(8, ["--gpus", "8", "--steps", "5"], 29555)
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=8" in cmd and "127.0.0.1" in cmd and cmd[-4:] == ["--gpus", "8", "--steps", "5"]
+    assert cmd[cmd.index("--master-port") + 1] == "29555"

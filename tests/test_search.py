@@ -50,3 +50,19 @@ def test_random_search_reaches_exhaustive_optimum(lengths):
     best = min(cost([ir.to_pointers(lengths, s)])[0][0] for s in ir.enumerate_schedules(lengths))
     res = search.random_search(cost, lengths, 400, p_max=sum(lengths) - 1, seed=0)
     assert res.best_lat == best
+
+
+def test_coordinate_descent_over_p_reaches_one_stage():
+    """Alg.1 with fixed P > 0 cannot return the all-concurrent schedule (no pointers); searching
+    P from 0 can (reading R18b): with a profiler whose latency grows with the stage count the
+    result is the 1-stage schedule"""
+    from paper_2111_14255_b200 import search as S
+
+    def prof(cands):
+        lat = [100.0 + 10 * (len(r[0]) if r else 0) + 0.001 * sum(map(sum, r)) for r in cands]
+        return np.array(lat, np.float32), np.zeros(len(cands), np.int32)
+    r = S.coordinate_descent(prof, [5, 7], P=2, rounds=1, m=4)
+    assert len(r.best_rho[0]) == 2
+    r = S.coordinate_descent_over_p(prof, [5, 7], (0, 1, 2), rounds=1, m=4)
+    assert r.best_rho == [[], []] and r.best_lat == 100.0
+    assert r.evaluations == 1 + 2 * (1 + 2 * 4)
