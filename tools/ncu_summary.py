@@ -1,6 +1,7 @@
 """Summarise ncu --set full captures of the executor into profiles/<round>_executor_ncu.json/.md.
 
   python tools/ncu_summary.py r01 c2=gpurun_out/full_c2.ncu-rep c3=... [launches=gpurun_out/launches.csv]
+  (a report may also be given as its `--page raw --csv` export, *.raw.csv)
 """
 import csv
 import io
@@ -44,7 +45,10 @@ for arg in sys.argv[2:]:
         out["launch_list"] = {"file": os.path.basename(path), "kernels": len(data),
                               "time_share": {n: round(v / s, 4) for n, v in sorted(tot.items(), key=lambda x: -x[1])}}
         continue
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):   # an `ncu -i X --page raw --csv` export (made on the GPU box)
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     for r in rows[2:]:
