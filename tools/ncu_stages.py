@@ -27,7 +27,10 @@ rnd = sys.argv[1]
 out = {}
 for arg in sys.argv[2:]:
     key, path = arg.split("=", 1)
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):   # an `ncu -i X --page raw --csv` export (made on the GPU box)
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     stages = []
