@@ -942,8 +942,12 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
 // ------------------------------------------------------------------------------------------
 template <typename T>
 __device__ void conv_simt_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_t *smem) {
-  float *As = reinterpret_cast<float *>(smem);                 // [BK][BM]
-  float *Bs = As + MT_SIMT_BK * MT_SIMT_BM;                    // [BK][BN]
+  // double-buffered K-blocks: As[2][BK][BM], Bs[2][BK][BN]; the gathers of K-block j+1 are in
+  // flight while K-block j's FMAs run.  A thread loads k = k0 + (tid & 15) for the four rows /
+  // output channels p0 + 16 i; the per-row gather bases are computed once per tile.  Same FMA
+  // order as a single-buffered loop (bit-identical results).
+  float *As = reinterpret_cast<float *>(smem);
+  float *Bs = As + 2 * MT_SIMT_BK * MT_SIMT_BM;
   const int tid = threadIdx.x;
   const int mt = tile / d.tiles_n, nt = tile - (tile / d.tiles_n) * d.tiles_n;
   const int m0 = mt * MT_SIMT_BM, n0 = nt * MT_SIMT_BN;
@@ -951,46 +955,67 @@ __device__ void conv_simt_tile(const RunArgs &a, const OpDesc &d, int tile, uint
   const float *Wt = reinterpret_cast<const float *>(d.w);
   const int HoWo = d.Ho * d.Wo;
   const int ty = tid >> 4, tx = tid & 15;
+  const int kk = tid & 15, p0 = tid >> 4;
+  int hb[4], wb[4], base[4];
+  bool rv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + p0 + 16 * i;
+    rv[i] = m < d.M;
+    const int mm = rv[i] ? m : 0;
+    const int n = mm / HoWo, rem = mm - n * HoWo;
+    const int ho = rem / d.Wo, wo = rem - ho * d.Wo;
+    base[i] = n * d.H;
+    hb[i] = ho * d.sh - d.ph;
+    wb[i] = wo * d.sw - d.pw;
+  }
+  float ra[4], rb[4];
+  auto load = [&](int k0) {
+    const int k = k0 + kk;
+    const bool kv = k < d.K;
+    const int tap = kv ? k / d.C : 0, ci = k - tap * d.C;
+    const int rr = tap / d.kw, ss = tap - rr * d.kw;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int hi = hb[i] + rr, wi = wb[i] + ss;
+      ra[i] = (kv && rv[i] && hi >= 0 && hi < d.H && wi >= 0 && wi < d.W)
+                  ? ld1_cg(X + ((int64_t)(base[i] + hi) * d.W + wi) * d.in_cs + d.in_co + ci)
+                  : 0.f;
+      const int co = n0 + p0 + 16 * i;
+      rb[i] = (kv && co < d.Co) ? __ldg(Wt + (int64_t)co * d.K + k) : 0.f;
+    }
+  };
   float acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  load(0);
+  int buf = 0;
   for (int k0 = 0; k0 < d.K; k0 += MT_SIMT_BK) {
+    float *Ab = As + buf * MT_SIMT_BK * MT_SIMT_BM, *Bb = Bs + buf * MT_SIMT_BK * MT_SIMT_BN;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int idx = tid + 256 * i;
-      const int kk = idx & 15, p = idx >> 4;
-      const int k = k0 + kk, m = m0 + p;
-      float v = 0.f;
-      if (k < d.K && m < d.M) {
-        const int tap = k / d.C, ci = k - tap * d.C;
-        const int rr = tap / d.kw, ss = tap - rr * d.kw;
-        const int n = m / HoWo, rem = m - n * HoWo;
-        const int ho = rem / d.Wo, wo = rem - ho * d.Wo;
-        const int hi = ho * d.sh - d.ph + rr, wi = wo * d.sw - d.pw + ss;
-        if (hi >= 0 && hi < d.H && wi >= 0 && wi < d.W)
-          v = ld1_cg(X + ((int64_t)(n * d.H + hi) * d.W + wi) * d.in_cs + d.in_co + ci);
-      }
-      As[kk * MT_SIMT_BM + p] = v;
-      const int co = n0 + p;
-      Bs[kk * MT_SIMT_BN + p] = (k < d.K && co < d.Co) ? __ldg(Wt + (int64_t)co * d.K + k) : 0.f;
+      Ab[kk * MT_SIMT_BM + p0 + 16 * i] = ra[i];
+      Bb[kk * MT_SIMT_BN + p0 + 16 * i] = rb[i];
     }
     __syncthreads();
+    if (k0 + MT_SIMT_BK < d.K) load(k0 + MT_SIMT_BK);
 #pragma unroll
-    for (int kk = 0; kk < MT_SIMT_BK; ++kk) {
+    for (int k2 = 0; k2 < MT_SIMT_BK; ++k2) {
       float av[4], bv[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) av[i] = As[kk * MT_SIMT_BM + ty * 4 + i];
+      for (int i = 0; i < 4; ++i) av[i] = Ab[k2 * MT_SIMT_BM + ty * 4 + i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk * MT_SIMT_BN + tx * 4 + j];
+      for (int j = 0; j < 4; ++j) bv[j] = Bb[k2 * MT_SIMT_BN + tx * 4 + j];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
-    __syncthreads();
+    buf ^= 1;
   }
+  __syncthreads();
   const float *sc = reinterpret_cast<const float *>(d.scale);
   const float *sf = reinterpret_cast<const float *>(d.shift);
 #pragma unroll
@@ -1204,8 +1229,11 @@ __device__ void dw3_tile(const RunArgs &a, const OpDesc &d, int tile, const uint
 template <typename T>
 __device__ void dw_tile(const RunArgs &a, const OpDesc &d, int tile, const uint8_t *smem, int cap) {
   if (dw3_staged(d, cap)) {
-    if (d.sh == 1) dw3_tile<T, 1, 4>(a, d, tile, smem);
-    else dw3_tile<T, 2, 2>(a, d, tile, smem);
+    // fp32 storage: shorter runs (an fp32 8-channel vector is 8 registers, bf16's is 4); the
+    // per-output tap order is the same for every run length, so results do not depend on it
+    constexpr int R1 = sizeof(T) == 4 ? 2 : 4, R2 = sizeof(T) == 4 ? 1 : 2;
+    if (d.sh == 1) dw3_tile<T, 1, R1>(a, d, tile, smem);
+    else dw3_tile<T, 2, R2>(a, d, tile, smem);
     return;
   }
   const T *X = in_ptr<T>(a, d);

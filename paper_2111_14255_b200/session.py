@@ -57,7 +57,8 @@ class TenantMix:
     # and bounded claim-ahead (R20), critical-path-first / round-robin / no stealing
     # (partition rule, claim depth, steal mode) triples tried by calibrate()
     KNOBS = ((0, 0, 2), (1, 0, 2), (1, 2, 2), (1, 3, 2), (0, 3, 2), (1, 3, 0), (1, 0, 1), (2, 2, 2),
-             (0, 2, 2), (1, 4, 2), (1, 2, 0))
+             (0, 2, 2), (1, 4, 2), (1, 2, 0), (1, 1, 2), (0, 1, 2), (2, 1, 2), (2, 3, 2), (2, 0, 2),
+             (0, 4, 2), (1, -2, 2), (1, -3, 2), (1, 5, 2))
 
     def calibrate(self, knobs=KNOBS, runs=7, rho=None):
         """Runtime-aware choice of the executor's scheduling knobs for this mix: the SM-partition
