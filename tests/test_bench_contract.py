@@ -35,11 +35,18 @@ def test_reference_arm_line():
 @pytest.mark.gpu
 def test_our_arm_line_short():
     d = _line(["--steps", "5", "--warmup", "3", "--n-cand", "16", "--search-cand", "8", "--no-cpu"], 900)
-    for k in KEYS + ("roofline", "gpu_launches", "clocks"):
+    for k in KEYS + ("roofline", "gpu_launches", "clocks", "batch8", "stage_roofline", "baselines_ms"):
         assert k in d, k
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] == 5
-    assert d["roofline"]["frac"] > 0 and d["roofline"]["peak"] > 0
-    assert d["profiling"]["candidates"] == 16
+    assert d["config"]["workload"].startswith("c4 (configs[3] b1)")          # the largest single-GPU config
+    assert d["roofline"]["frac"] > 0 and d["roofline"]["peak"] > 0 and d["roofline"]["bound"] == "hbm"
+    assert len(d["stage_roofline"]) == d["config"]["stages"] and all(0 < s["frac"] <= 1 for s in d["stage_roofline"])
+    b8 = d["batch8"]
+    assert b8["workload"].startswith("c4b8") and b8["value"] > d["value"] and b8["roofline"]["bound"] == "tensor"
+    # sequential baseline with single-tenant plans is reported next to the mix-plan one
+    assert d["baselines_ms"]["seq_graph_single_tenant_plans"] > 0
+    assert d["profiling"]["candidates"] == 16 and 0 < d["profiling"]["frac_of_roofline"] < 1
+    assert d["profiling"]["search"]["best_P"] >= 0
 
 
 @pytest.mark.parametrize("config,sched,expect_us,tol", [
