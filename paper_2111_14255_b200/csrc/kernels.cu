@@ -1156,26 +1156,26 @@ __device__ void dw3_tile(const RunArgs &a, const OpDesc &d, int tile, const uint
     const int n = gr / d.Ho, ho = gr - n * d.Ho;
     const int wo0 = seg * RUN;
     const int wi0 = wo0 * S - d.pw;
-    const T *xb = X + (int64_t)n * H * W * cs + d.in_co + g * 8;
+    const T *xrow = X + (int64_t)n * H * W * cs + d.in_co + g * 8;
     float2 acc[RUN][4];
 #pragma unroll
     for (int o = 0; o < RUN; ++o)
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[o][q] = make_float2(0.f, 0.f);
-    Raw8<T> xr[3][NC];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {   // every load of the item issued before any arithmetic
+    // rolling two-row window: rows 0 and 1 are loaded up front, row 2 into row 0's registers once
+    // row 0 is consumed (two thirds of the registers of loading all three rows, which set the
+    // executor's register peak); taps are still accumulated in (r, s) order
+    Raw8<T> xa[NC], xb[NC];
+    auto load_row = [&](int r, Raw8<T> *dst) {
       const int hi = ho * S - d.ph + r;
       const bool rok = hi >= 0 && hi < H;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         const int wi = wi0 + c;
-        xr[r][c] = ldraw_cg_pred(xb + (int64_t)(hi * W + wi) * cs, rok && wi >= 0 && wi < W);
+        dst[c] = ldraw_cg_pred(xrow + (int64_t)(hi * W + wi) * cs, rok && wi >= 0 && wi < W);
       }
-    }
-    if (threadIdx.x == 0 && it == 0) { const uint32_t u = raw_word(xr[2][NC - 1]); sh_t_load_dw = gtimer() + (u == 0x7fff1234u); }
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
+    };
+    auto mac_row = [&](int r, const Raw8<T> *src) {
       float2 w2[3][4];   // this kernel row's 3 taps (fp32 weights, [9][C])
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
@@ -1187,7 +1187,7 @@ __device__ void dw3_tile(const RunArgs &a, const OpDesc &d, int tile, const uint
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         float2 x[4];
-        cvt8x2(xr[r][c], x);
+        cvt8x2(src[c], x);
 #pragma unroll
         for (int s2 = 0; s2 < 3; ++s2) {
           // column c feeds output o when o*S + s2 == c
@@ -1198,7 +1198,14 @@ __device__ void dw3_tile(const RunArgs &a, const OpDesc &d, int tile, const uint
           }
         }
       }
-    }
+    };
+    load_row(0, xa);
+    load_row(1, xb);
+    if (threadIdx.x == 0 && it == 0) { const uint32_t u = raw_word(xb[NC - 1]); sh_t_load_dw = gtimer() + (u == 0x7fff1234u); }
+    mac_row(0, xa);
+    load_row(2, xa);
+    mac_row(1, xb);
+    mac_row(2, xa);
     float2 sc2[4], sf2[4];
     {
       const float4 a0 = reinterpret_cast<const float4 *>(sc + g * 8)[0];
