@@ -581,7 +581,9 @@ __device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const Conv
         tc_mma(tmem, ad + a_k, bd + 2, idesc, 1u);
         tc_mma(tmem, ad + 2 * a_k, bd + 4, idesc, 1u);
         tc_mma(tmem, ad + 3 * a_k, bd + 6, idesc, 1u);
-        tc_commit(bar_empty0 + 8 * s);
+        // the empty barrier only tracks reuse within the tile: a stage's last use is covered by
+        // the accumulator commit, so no mbarrier phase completes without a waiter (synccheck)
+        if (i + nst < nk) tc_commit(bar_empty0 + 8 * s);
       }
       __syncwarp();
       ad += st16;
@@ -667,7 +669,7 @@ __device__ __forceinline__ void conv_tc_mainloop_cpasync(const RunArgs &a, const
         for (int kk = 0; kk < MT_BK / 16; ++kk)
           tc_mma(tmem, sdesc_sw128(ab + kk * 32), sdesc_sw128(bb + kk * 32), idesc,
                  (j > 0 || kk > 0) ? 1u : 0u);
-        tc_commit(bar_empty0 + 8 * s);        // frees the smem stage when these MMAs complete
+        if (j + MT_STAGES < nk) tc_commit(bar_empty0 + 8 * s);   // frees the stage for its reuse
         if (j == nk - 1) tc_commit(bar_accf);  // accumulator complete
       }
     }
@@ -814,13 +816,12 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
   const uint32_t bar_accf = smem_u32(&sh.bar_accf);
   if (d.tma) conv_tc_mainloop_tma(d, ct, smem, sh, ps);
   else conv_tc_mainloop_cpasync(a, d, ct, smem, sh, ps);
-  {   // stage s was used ceil((nk - s) / nst) times: flip its parities when odd
+  {   // stage s was used u = ceil((nk - s) / nst) times: full completed u times, empty u - 1
     const int nst = d.tma ? d.nst : MT_STAGES;
     for (int st = 0; st < nst && st < ct.nk; ++st) {
-      if ((((ct.nk - 1 - st) / nst) & 1) == 0) {
-        ps.eph ^= 1u << st;
-        if (d.tma) ps.fph ^= 1u << st;
-      }
+      const int u1 = (ct.nk - 1 - st) / nst;   // u - 1
+      if (u1 & 1) ps.eph ^= 1u << st;
+      if (d.tma && (u1 & 1) == 0) ps.fph ^= 1u << st;
     }
   }
   if (tid < 64) mbar_wait(bar_accf, ps.acc_phase);
