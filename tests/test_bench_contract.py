@@ -22,7 +22,7 @@ def _line(args, timeout):
 
 
 def test_reference_arm_line():
-    d = _line(["--impl", "reference", "--steps", "2", "--warmup", "1"], 900)
+    d = _line(["--impl", "reference", "--steps", "2", "--warmup", "1", "--config", "c2"], 900)
     assert d["impl"] == "reference"
     assert d["steps"] == 2 and d["warmup"] == 1          # K timed steps after W untimed ones
     for k in KEYS:
