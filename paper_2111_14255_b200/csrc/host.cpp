@@ -26,6 +26,35 @@ static const int64_t TC_GFLOPS = 2250000;  // spec dense bf16 GFLOP/s (2.25 PFLO
 static constexpr double TMA_BPUS = 160000.0;
 static const int64_t MT_HOP_NS = 2000;   // partition mode 2: dependency hop between ops (traces)
 static constexpr int BN_MIN = 32;        // narrowest N tile the cost model considers
+// K-blocks per ring stage of the TMA conv mainloop.  The producer and MMA-issuer loops run on one
+// thread each, and per ring stage they pay a dependent chain of barrier probe, expect_tx / commit
+// and descriptor moves of ~250 ns (tools/kb_pipe.cu, tools/loop_bisect.cu) -- more than the TMA
+// transfer or the UMMAs of one 64-wide k-block at batch-1 tile sizes.  Grouping kg k-blocks under
+// one barrier pair amortises that chain; kg = 2 is taken when it still leaves MT_KG_MIN_NST stages
+// in the ring (kg = 4 measured the same end to end; each kg is one more mainloop instantiation).
+// Only the pipeline's granularity changes: the UMMAs and their order are the same, so outputs are
+// bit-identical for every kg.
+#ifndef MT_KG_MIN_NST
+#define MT_KG_MIN_NST 3
+#endif
+#ifndef MT_KG_MAX
+#define MT_KG_MAX 2   // the device mainloop is instantiated for kg = 1 and 2
+#endif
+// The UMMA reads all 128 rows (16 KB) of an A sub-block even when the box holds fewer output
+// pixels (e.g. 25 at 5x5): the rows past the box are discarded by the epilogue, but the read must
+// stay inside the ring, so the last sub-block needs (16 KB - A region) bytes of slack behind it.
+#ifndef MT_KB_OVH
+#define MT_KB_OVH 0.0   // cost model: us of issue-chain latency per ring stage (divided over its kg k-blocks)
+#endif
+static int ring_slack(int st_boff) { return std::max(0, MT_BM * 128 - st_boff); }
+static int kgroup(int st_bytes, int st_boff, int kb_per_split) {
+  for (int kg = MT_KG_MAX; kg > 1; kg >>= 1)
+    if (kb_per_split >= 2 * kg && (MT_PIPE_BYTES - ring_slack(st_boff)) / (kg * st_bytes) >= MT_KG_MIN_NST) return kg;
+  return 1;
+}
+static int ring_stages(int st_bytes, int st_boff, int kg) {
+  return std::min(MT_MAXST, (MT_PIPE_BYTES - ring_slack(st_boff)) / (kg * st_bytes));
+}
 
 struct mt_ctx {
   int device = -1;
@@ -454,10 +483,12 @@ static mt_status plan_graphs(mt_ctx *c) {
               const int bn_min = BN_MIN;
               for (int bn = bn_max; bn >= bn_min || bn == bn_max; bn >>= 1) {
                 const int64_t tn = cdiv(os.c, bn), tmn_c = (int64_t)d.tiles_m * tn;
-                const double t_kb = std::max(0.13 * bn / 128.0, (a_kb + bn * 128.0) / TMA_BPUS);
+                const int boff = d.tma == 2 ? 16 * 1024 : (int)rup(d.a_bytes, 1024);
                 for (int sp = 1; sp <= 12; ++sp) {
                   if (sp > 1 && d.nkb / sp < 2) break;
                   const int64_t kbps = cdiv(d.nkb, sp);
+                  const int kgb = d.tma ? kgroup(boff + (int)rup(bn * 128, 1024), boff, (int)kbps) : 1;
+                  const double t_kb = std::max(0.13 * bn / 128.0, (a_kb + bn * 128.0) / TMA_BPUS) + MT_KB_OVH / kgb;
                   const int64_t waves = cdiv(tmn_c * sp, sm_avail);
                   double t = waves * (1.3 + kbps * t_kb + (sp == 1 ? 1.3 + 0.01 * bn : 0.6));
                   if (sp > 1) {
@@ -478,10 +509,12 @@ static mt_status plan_graphs(mt_ctx *c) {
             if (d.tma) {   // pipeline depth from the real box sizes (SW128 needs 1 KB alignment)
               d.st_boff = d.tma == 2 ? 16 * 1024 : (int)rup(d.a_bytes, 1024);
               d.st_bytes = d.st_boff + (int)rup(d.bn * 128, 1024);
-              d.nst = std::min(MT_MAXST, MT_PIPE_BYTES / d.st_bytes);
+              d.kg = kgroup(d.st_bytes, d.st_boff, d.kb_per_split);
+              d.nst = ring_stages(d.st_bytes, d.st_boff, d.kg);
             } else {
               d.st_boff = 16 * 1024;
               d.st_bytes = 32 * 1024;
+              d.kg = 1;
               d.nst = MT_STAGES;
             }
             d.tiles = tmn * d.splits + tmn * d.rc;
@@ -547,7 +580,8 @@ static mt_status plan_graphs(mt_ctx *c) {
             d.rc = d.splits > 1 ? 1 : 0;
             d.st_boff = d.a_bytes;
             d.st_bytes = d.st_boff + (int)rup(d.bn * 128, 1024);
-            d.nst = std::min(MT_MAXST, MT_PIPE_BYTES / d.st_bytes);
+            d.kg = kgroup(d.st_bytes, d.st_boff, d.kb_per_split);
+            d.nst = ring_stages(d.st_bytes, d.st_boff, d.kg);
             d.tiles = (int)(tmn * d.splits + tmn * d.rc);
             if (d.splits > 1) {
               d.cnt_off = split_cnt;
@@ -615,7 +649,8 @@ static mt_status plan_graphs(mt_ctx *c) {
     if (d.tk == TK_CONV_TC) {
       const double a_kb = d.tma ? (double)d.a_bytes : 16384.0;
       const double rows = d.tma == 3 ? 128.0 : d.tma ? (double)d.blk_rows * d.seg_w : 128.0;
-      const double t_kb = std::max(0.13 * d.bn / 128.0, (a_kb + d.bn * 128.0) / TMA_BPUS);
+      const double t_kb = std::max(0.13 * d.bn / 128.0, (a_kb + d.bn * 128.0) / TMA_BPUS) +
+                          MT_KB_OVH / std::max(1, (int)d.kg);
       const int64_t tmn = (int64_t)d.tiles_m * d.tiles_n;
       t0 = tmn * d.splits;
       us0 = 1.3 + d.kb_per_split * t_kb + (d.splits == 1 ? 1.3 + 0.01 * d.bn : 0.6);

@@ -451,12 +451,20 @@ __device__ void conv_tc_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaSh
       asm volatile("prefetch.tensormap [%0];" ::"l"(d.tmap_a) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(d.tmap_b) : "memory");
       const uint32_t bar_full0 = smem_u32(&sh.bar_full[0]);
-      for (int i = 0; i < d.nst && i < ct.nk; ++i) {
-        mbar_expect_tx(bar_full0 + 8 * i, (uint32_t)(d.a_bytes + d.bn * 128));
-        if (d.tma == 3)   // FC: the weights are the A (M = features) operand
-          tma_load_2d(s0 + i * d.st_bytes, d.tmap_a, bar_full0 + 8 * i, (ct.kb0 + i) * MT_BK, ct.m0);
-        else
-          tma_load_2d(s0 + i * d.st_bytes + d.st_boff, d.tmap_b, bar_full0 + 8 * i, (ct.kb0 + i) * MT_BK, ct.n0);
+      const int kg = d.kg;
+      const uint32_t txb = (uint32_t)(d.a_bytes + d.bn * 128);
+      // ring stage i holds k-blocks [i*kg, min(nk, (i+1)*kg)) as kg consecutive sub-blocks
+      for (int i = 0, kb = 0; i < d.nst && kb < ct.nk; ++i) {
+        const int g = min(kg, ct.nk - kb);
+        const uint32_t bar = bar_full0 + 8 * i;
+        mbar_expect_tx(bar, txb * (uint32_t)g);
+        for (int u = 0; u < g; ++u, ++kb) {
+          const uint32_t sub = s0 + (uint32_t)(kb * d.st_bytes);
+          if (d.tma == 3)   // FC: the weights are the A (M = features) operand
+            tma_load_2d(sub, d.tmap_a, bar, (ct.kb0 + kb) * MT_BK, ct.m0);
+          else
+            tma_load_2d(sub + d.st_boff, d.tmap_b, bar, (ct.kb0 + kb) * MT_BK, ct.n0);
+        }
       }
     }
   } else {
@@ -487,9 +495,10 @@ __device__ void conv_tc_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaSh
     sh.esh[tid] = n < d.Co ? __ldg(reinterpret_cast<const float *>(d.shift) + n) : 0.f;
   }
   // the rest of this split's weight rows -> L2 (one bulk prefetch per row)
-  if (ct.nk > d.nst && tid < d.bn)
-    prefetch_l2_bulk(Wt + (int64_t)(ct.n0 + tid) * d.Kpad + (ct.kb0 + d.nst) * MT_BK,
-                     (uint32_t)(ct.nk - d.nst) * MT_BK * 2);
+  const int kpre = d.tma ? d.nst * d.kg : MT_STAGES;   // k-blocks whose weights are already requested
+  if (ct.nk > kpre && tid < d.bn)
+    prefetch_l2_bulk(Wt + (int64_t)(ct.n0 + tid) * d.Kpad + (ct.kb0 + kpre) * MT_BK,
+                     (uint32_t)(ct.nk - kpre) * MT_BK * 2);
 }
 
 __device__ __forceinline__ bool elect_one() {
@@ -499,9 +508,16 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 // TMA mainloop.  Warp 0 = producer (A boxes, and B beyond the prefetched stages), warp 1 = MMA
-// issuer (UMMA 128 x bn x 16 from a stage's two tiles; commit frees the stage); both loops run
-// warp-wide with one elected lane issuing, descriptors are precomputed and advanced by adds.
-// Everyone else waits for the accumulator.
+// issuer (UMMA 128 x bn x 16 from a sub-block's two tiles; commit frees the ring stage).  A ring
+// stage holds KG (1 or 2) consecutive k-blocks (sub-blocks st_bytes apart) behind one full / empty
+// barrier pair, so the per-stage chain of single-thread latencies (barrier probe, expect_tx or
+// commit, warp reconvergence, ~250 ns; tools/kb_pipe.cu) is paid once per KG k-blocks.  KG is a
+// template parameter with the sub-block loop unrolled: a runtime-trip-count inner loop measured 10 %
+// slower end to end (the issue state leaves the uniform datapath), and so did one 4-slot body
+// predicated by a runtime kg (kg = 1 ops paid for the dead slots).  A tile's tail stage holds
+// g <= KG k-blocks.  Both loops run warp-wide with one elected lane issuing; everyone else waits
+// for the accumulator.
+template <int KG>
 __device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const ConvTile &ct, uint8_t *smem,
                                                      CtaShared &sh, const PipeState &ps) {
   const int warp = threadIdx.x >> 5;
@@ -510,6 +526,7 @@ __device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const Conv
   const uint32_t bar_empty0 = smem_u32(&sh.bar_empty[0]);
   const uint32_t bar_accf = smem_u32(&sh.bar_accf);
   const int nst = d.nst, nk = ct.nk, st_bytes = d.st_bytes, st_boff = d.st_boff;
+  const int nsq = KG == 1 ? nk : (nk + KG - 1) / KG;   // ring stages this tile fills
   if (warp == 0) {
     const uint32_t txb = (uint32_t)(d.a_bytes + d.bn * 128);
     const uint64_t tmap_a = d.tmap_a, tmap_b = d.tmap_b;
@@ -519,45 +536,60 @@ __device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const Conv
     int rr = tap / kw, ss = tap - rr * kw;
     const int hbase = ct.ho0 * d.sh - d.ph, wbase = ct.wo0 * d.sw - pw;
     const uint32_t eph = ps.eph;
-    int s = 0, j = 0;
+    int s = 0, j = 0, kb = kb0;
     uint32_t st = s0;
     fence_proxy_async_global();   // dependencies acquired (generic proxy) -> TMA reads (async proxy)
-    for (int i = 0; i < nk; ++i) {
+    for (int q = 0; q < nsq; ++q) {
       if (j > 0) mbar_wait(bar_empty0 + 8 * s, ((eph >> s) & 1u) ^ (uint32_t)((j - 1) & 1));
+      const int g = KG == 1 ? 1 : min(KG, kb0 + nk - kb);
       if (elect_one()) {
         const uint32_t bar = bar_full0 + 8 * s;
-        if (fc) {   // FC: weights (A slot) prefetched for the first nst k-blocks; input -> B slot
-          if (j > 0) {
-            mbar_expect_tx(bar, txb);
-            tma_load_2d(st, tmap_a, bar, (kb0 + i) * MT_BK, m0);
+        if (j > 0) mbar_expect_tx(bar, KG == 1 ? txb : txb * (uint32_t)g);
+        int c2 = cb, s2 = ss, r2 = rr;
+#pragma unroll
+        for (int u = 0; u < KG; ++u) {
+          if (KG == 1 || u < g) {
+            const uint32_t sub = st + (uint32_t)(u * st_bytes);
+            const int kbu = kb + u;
+            if (fc) {   // FC: weights (A slot) prefetched for the first nst stages; input -> B slot
+              if (j > 0) tma_load_2d(sub, tmap_a, bar, kbu * MT_BK, m0);
+              tma_load_2d(sub + st_boff, tmap_b, bar, kbu * MT_BK, n0);
+            } else {
+              if (j > 0) tma_load_2d(sub + st_boff, tmap_b, bar, kbu * MT_BK, n0);
+              if (small) {   // 8 taps x 8 channels: one 16-byte-row box per tap, 2 KB apart
+                int t8 = kbu * 8;
+                for (int tt = 0; tt < 8; ++tt, ++t8) {
+                  const int ra = t8 / kw, sa = t8 - ra * kw;
+                  const bool v = t8 < ntap;   // missing taps: an out-of-range box is zero-filled
+                  tma_load_4d(sub + tt * 2048, tmap_a, bar, 0, v ? wbase + sa : -(1 << 20), v ? hbase + ra : 0, img);
+                }
+              } else {
+                tma_load_4d(sub, tmap_a, bar, c2 * 64, wbase + s2, hbase + r2, img);
+              }
+            }
+            if (KG > 1 && ++c2 == cblks) {
+              c2 = 0;
+              if (++s2 == kw) { s2 = 0; ++r2; }
+            }
           }
-          tma_load_2d(st + st_boff, tmap_b, bar, (kb0 + i) * MT_BK, n0);
-        } else if (j > 0) {
-          mbar_expect_tx(bar, txb);
-          tma_load_2d(st + st_boff, tmap_b, bar, (kb0 + i) * MT_BK, n0);
         }
-        if (fc) {
-        } else if (small) {   // 8 taps x 8 channels: one 16-byte-row box per tap, 2 KB apart
-          int t8 = (kb0 + i) * 8;
-          for (int tt = 0; tt < 8; ++tt, ++t8) {
-            const int r2 = t8 / kw, s2 = t8 - r2 * kw;
-            const bool v = t8 < ntap;   // missing taps: an out-of-range box is zero-filled
-            tma_load_4d(st + tt * 2048, tmap_a, bar, 0, v ? wbase + s2 : -(1 << 20), v ? hbase + r2 : 0, img);
-          }
-        } else {
-          tma_load_4d(st, tmap_a, bar, cb * 64, wbase + ss, hbase + rr, img);
-        }
-        if (sh.tracing && (i == 0 || i == nk - 1)) {   // producer issue stamps (trace only)
-          if (i == 0) sh.t_is[0] = gtimer();
-          if (i == nk - 1) sh.t_aissue = gtimer();
+        if (sh.tracing && (q == 0 || q == nsq - 1)) {   // producer issue stamps (trace only)
+          if (q == 0) sh.t_is[0] = gtimer();
+          if (q == nsq - 1) sh.t_aissue = gtimer();
         }
       }
       __syncwarp();
-      if (++cb == cblks) {
-        cb = 0;
-        if (++ss == kw) { ss = 0; ++rr; }
+#pragma unroll
+      for (int u = 0; u < KG; ++u) {
+        if (KG == 1 || u < g) {
+          if (++cb == cblks) {
+            cb = 0;
+            if (++ss == kw) { ss = 0; ++rr; }
+          }
+        }
       }
-      st += st_bytes;
+      kb += g;
+      st += (uint32_t)(KG * st_bytes);
       if (++s == nst) { s = 0; ++j; st = s0; }
     }
   } else if (warp == 1) {
@@ -565,29 +597,37 @@ __device__ __forceinline__ void conv_tc_mainloop_tma(const OpDesc &d, const Conv
     const uint32_t tmem = sh.tmem_base;
     const uint32_t fph = ps.fph;
     const bool small = d.tma == 2;
-    // descriptors of stage 0; a stage advances the start-address field by st_bytes/16, one MMA K
-    // step by 32 B (SW128: +2) or 2 x 2 KB (no swizzle: +256)
+    // descriptors of stage 0; a sub-block advances the start-address field by st_bytes/16, a ring
+    // stage by KG*st_bytes/16, one MMA K step by 32 B (SW128: +2) or 2 x 2 KB (no swizzle: +256)
     const uint64_t ad0 = small ? sdesc_noswz(s0, 2048, 128) : sdesc_sw128(s0);
     const uint64_t bd0 = sdesc_sw128(s0 + st_boff);
-    const uint64_t a_k = small ? 256 : 2, st16 = (uint64_t)(st_bytes >> 4);
+    const uint64_t a_k = small ? 256 : 2, sub16 = (uint64_t)(st_bytes >> 4), stg16 = (uint64_t)KG * sub16;
     uint64_t ad = ad0, bd = bd0;
-    int s = 0, j = 0;
-    for (int i = 0; i < nk; ++i) {
+    int s = 0, j = 0, kb = 0;
+    for (int q = 0; q < nsq; ++q) {
       mbar_wait(bar_full0 + 8 * s, ((fph >> s) & 1u) ^ (uint32_t)(j & 1));
       tc_fence_after();
+      const int g = KG == 1 ? 1 : min(KG, nk - kb);
       if (elect_one()) {
-        if (i == 0) sh.t_first = gtimer();
-        tc_mma(tmem, ad, bd, idesc, i > 0 ? 1u : 0u);
-        tc_mma(tmem, ad + a_k, bd + 2, idesc, 1u);
-        tc_mma(tmem, ad + 2 * a_k, bd + 4, idesc, 1u);
-        tc_mma(tmem, ad + 3 * a_k, bd + 6, idesc, 1u);
+        if (q == 0) sh.t_first = gtimer();
+#pragma unroll
+        for (int u = 0; u < KG; ++u) {
+          if (KG == 1 || u < g) {
+            const uint64_t a = ad + u * sub16, b = bd + u * sub16;
+            tc_mma(tmem, a, b, idesc, (kb + u) > 0 ? 1u : 0u);
+            tc_mma(tmem, a + a_k, b + 2, idesc, 1u);
+            tc_mma(tmem, a + 2 * a_k, b + 4, idesc, 1u);
+            tc_mma(tmem, a + 3 * a_k, b + 6, idesc, 1u);
+          }
+        }
         // the empty barrier only tracks reuse within the tile: a stage's last use is covered by
         // the accumulator commit, so no mbarrier phase completes without a waiter (synccheck)
-        if (i + nst < nk) tc_commit(bar_empty0 + 8 * s);
+        if (q + nst < nsq) tc_commit(bar_empty0 + 8 * s);
       }
       __syncwarp();
-      ad += st16;
-      bd += st16;
+      kb += g;
+      ad += stg16;
+      bd += stg16;
       if (++s == nst) { s = 0; ++j; ad = ad0; bd = bd0; }
     }
     if (elect_one()) {
@@ -814,12 +854,16 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
   const ConvTile ct = conv_tile_coords(d, tile);
   const int tmn = ct.tmn, ks = ct.ks, n0 = ct.n0;
   const uint32_t bar_accf = smem_u32(&sh.bar_accf);
-  if (d.tma) conv_tc_mainloop_tma(d, ct, smem, sh, ps);
+  if (d.tma) {
+    if (d.kg == 2) conv_tc_mainloop_tma<2>(d, ct, smem, sh, ps);
+    else conv_tc_mainloop_tma<1>(d, ct, smem, sh, ps);
+  }
   else conv_tc_mainloop_cpasync(a, d, ct, smem, sh, ps);
-  {   // stage s was used u = ceil((nk - s) / nst) times: full completed u times, empty u - 1
+  {   // ring stage s was used u = ceil((nsq - s) / nst) times: full completed u times, empty u - 1
     const int nst = d.tma ? d.nst : MT_STAGES;
-    for (int st = 0; st < nst && st < ct.nk; ++st) {
-      const int u1 = (ct.nk - 1 - st) / nst;   // u - 1
+    const int nsq = d.tma ? (ct.nk + d.kg - 1) / d.kg : ct.nk;   // ring stages filled by this tile
+    for (int st = 0; st < nst && st < nsq; ++st) {
+      const int u1 = (nsq - 1 - st) / nst;   // u - 1
       if (u1 & 1) ps.eph ^= 1u << st;
       if (d.tma && (u1 & 1) == 0) ps.fph ^= 1u << st;
     }

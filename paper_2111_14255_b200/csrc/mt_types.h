@@ -63,8 +63,9 @@ struct OpDesc {
   int32_t a_bytes;                  // TMA: bytes of one A box (rows * Wo * 128)
   int32_t rc;                       // split-K: reduce tiles per (M,N) tile (32 columns each); the op's
                                     // tiles are [tmn*splits compute tiles][tmn*rc reduce tiles]
-  int32_t nst;                      // conv pipeline: stages, bytes per stage, offset of B in a stage
-  int32_t st_bytes, st_boff, pad3;
+  int32_t nst;                      // conv pipeline: ring stages; bytes of one k-block's (A box + B box)
+  int32_t st_bytes, st_boff, kg;    // sub-block, offset of B in it; kg = k-blocks per ring stage (one
+                                    // full/empty barrier pair, expect_tx and commit per kg k-blocks)
   int32_t M, K, Kpad, nkb;          // GEMM view (conv / FC)
   int32_t bn, tiles_m, tiles_n, splits;
   int32_t kb_per_split, tiles, cnt_off, pad0;

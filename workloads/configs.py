@@ -41,6 +41,8 @@ CONFIGS = {
     "r18": (("resnet18",), 1, zoo.PREC_BF16, "ResNet-18 alone"),
     "r50": (("resnet50",), 1, zoo.PREC_BF16, "ResNet-50 alone"),
     "vgg": (("vgg16",), 1, zoo.PREC_BF16, "VGG-16 alone"),
+    "inc3": (("inception_v3",), 1, zoo.PREC_BF16, "Inception-v3 alone"),
+    "sqz": (("squeezenet1_0",), 1, zoo.PREC_BF16, "SqueezeNet 1.0 alone"),
     "vgg_b8": (("vgg16",), 8, zoo.PREC_BF16, "VGG-16 alone, batch 8"),
 }
 
