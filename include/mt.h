@@ -118,7 +118,15 @@ typedef enum {
                            /* 2 (default): ... the tenant with most unclaimed ops first     */
   MT_OPT_NUM_SMS = 2,      /* host-only contexts: SM count used for the partition (148)    */
   MT_OPT_TIMEOUT_MS = 3,   /* device spin timeout (default 2000 ms)                         */
-  MT_OPT_CTAS_PER_SM = 4,  /* reserved (1)                                                  */
+  MT_OPT_CTAS_PER_SM = 4,  /* 1 (default): one 256-thread executor CTA per SM, 192 KB conv  */
+                           /* ring.  2: heterogeneous co-residency:  */
+                           /* two 128-thread CTAs per SM (96 KB ring, 256 TMEM columns      */
+                           /* each); slot 0 of every SM serves the stage's SM partition from */
+                           /* the most to the least compute-intense tenant, slot 1 the same  */
+                           /* list reversed, pairing compute- and memory-bound slices on one */
+                           /* SM.  Plans depend on it: set before mt_load_graphs           */
+                           /* (MT_ERR_STATE after); bf16 tenants only (MT_ERR_REFUSED at     */
+                           /* load for fp32); MT_ERR_REFUSED if the build does not fit.     */
   MT_OPT_PARTITION = 5,    /* SM partition rule per stage (a3; R16 / R16b):       */
                            /* 0 (default): n_t proportional to the slice's roofline time    */
                            /*    (north star); 1: latency-balanced -- minimise max_t E_t,   */

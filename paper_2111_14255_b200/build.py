@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmt.so")
-SOURCES = ["kernels.cu", "host.cpp", "plan.cpp"]
+SOURCES = ["kernels.cu", "kernels_cr.cu", "host.cpp", "plan.cpp"]
 HEADERS = ["kernels.h", "mt_types.h", "plan.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -47,13 +47,13 @@ static constexpr int BN_MIN = 32;        // narrowest N tile the cost model cons
 #define MT_KB_OVH 0.0   // cost model: us of issue-chain latency per ring stage (divided over its kg k-blocks)
 #endif
 static int ring_slack(int st_boff) { return std::max(0, MT_BM * 128 - st_boff); }
-static int kgroup(int st_bytes, int st_boff, int kb_per_split) {
+static int kgroup(int pipe, int st_bytes, int st_boff, int kb_per_split) {
   for (int kg = MT_KG_MAX; kg > 1; kg >>= 1)
-    if (kb_per_split >= 2 * kg && (MT_PIPE_BYTES - ring_slack(st_boff)) / (kg * st_bytes) >= MT_KG_MIN_NST) return kg;
+    if (kb_per_split >= 2 * kg && (pipe - ring_slack(st_boff)) / (kg * st_bytes) >= MT_KG_MIN_NST) return kg;
   return 1;
 }
-static int ring_stages(int st_bytes, int st_boff, int kg) {
-  return std::min(MT_MAXST, (MT_PIPE_BYTES - ring_slack(st_boff)) / (kg * st_bytes));
+static int ring_stages(int pipe, int st_bytes, int st_boff, int kg) {
+  return std::min(MT_MAXST, (pipe - ring_slack(st_boff)) / (kg * st_bytes));
 }
 
 struct mt_ctx {
@@ -65,6 +65,10 @@ struct mt_ctx {
   int claim_depth = 0; // MT_OPT_CLAIM_DEPTH
   int stage_split = 0; // MT_OPT_STAGE_SPLIT
   int partition = 0;   // MT_OPT_PARTITION: 0 roofline-proportional, 1 latency-balanced, 2 work/span
+  int cps = 1;         // MT_OPT_CTAS_PER_SM: 1 (mtk build) or 2 (co-resident mtk_cr build, f4)
+  // device-code configuration the plans are made for (mt_types.h)
+  int nthreads() const { return cps == 2 ? 128 : 256; }
+  int pipe_bytes() const { return cps == 2 ? MT_PIPE_BYTES_2 : MT_PIPE_BYTES_1; }
   int64_t timeout_ms = 2000;
   bool loaded = false, bound = false, has_sched = false;
   std::vector<Tenant> T;
@@ -90,6 +94,17 @@ struct mt_ctx {
   int64_t trace_cap = 0;
   float *g_out[8][MT_MAXT] = {};
 };
+
+// launch interface of the device build a context plans for (1 or 2 CTAs per SM)
+static cudaError_t k_executor(const mt_ctx *c, const RunArgs &a, int grid, cudaStream_t s) {
+  return c->cps == 2 ? mtk_cr::launch_executor(a, grid, s) : mtk::launch_executor(a, grid, s);
+}
+static cudaError_t k_op(const mt_ctx *c, const RunArgs &a, const OpDesc &d, int op, int max_grid, cudaStream_t s) {
+  return c->cps == 2 ? mtk_cr::launch_op(a, d, op, max_grid, s) : mtk::launch_op(a, d, op, max_grid, s);
+}
+static cudaError_t k_pack(const mt_ctx *c, const RunArgs &a, int t, cudaStream_t s) {
+  return c->cps == 2 ? mtk_cr::launch_pack(a, t, s) : mtk::launch_pack(a, t, s);
+}
 
 // cached baseline graphs capture RunArgs (workspace, trace buffer, timeout): drop them whenever
 // one of those changes
@@ -418,10 +433,10 @@ static mt_status plan_graphs(mt_ctx *c) {
               // whole output rows per tile (row-run kernel): ~MT_NTHREADS*1.5 items per tile
               const int run = n.sh == 1 ? 4 : 2;
               const int64_t per_row = cdiv(os.w, run) * (os.c / 8);
-              const int rows = (int)std::max<int64_t>(1, MT_NTHREADS / per_row);
+              const int rows = (int)std::max<int64_t>(1, c->nthreads() / per_row);
               d.pix_tile = rows * os.w;
             } else {
-              d.pix_tile = (int)std::max<int64_t>(1, (MT_NTHREADS * MT_EW_PER_THREAD) / (os.c / 8));
+              d.pix_tile = (int)std::max<int64_t>(1, (c->nthreads() * MT_EW_PER_THREAD) / (os.c / 8));
             }
             d.tiles = (int)cdiv((int64_t)g.batch * os.h * os.w, d.pix_tile);
             wp.mode = 3;
@@ -487,7 +502,7 @@ static mt_status plan_graphs(mt_ctx *c) {
                 for (int sp = 1; sp <= 12; ++sp) {
                   if (sp > 1 && d.nkb / sp < 2) break;
                   const int64_t kbps = cdiv(d.nkb, sp);
-                  const int kgb = d.tma ? kgroup(boff + (int)rup(bn * 128, 1024), boff, (int)kbps) : 1;
+                  const int kgb = d.tma ? kgroup(c->pipe_bytes(), boff + (int)rup(bn * 128, 1024), boff, (int)kbps) : 1;
                   const double t_kb = std::max(0.13 * bn / 128.0, (a_kb + bn * 128.0) / TMA_BPUS) + MT_KB_OVH / kgb;
                   const int64_t waves = cdiv(tmn_c * sp, sm_avail);
                   double t = waves * (1.3 + kbps * t_kb + (sp == 1 ? 1.3 + 0.01 * bn : 0.6));
@@ -509,8 +524,8 @@ static mt_status plan_graphs(mt_ctx *c) {
             if (d.tma) {   // pipeline depth from the real box sizes (SW128 needs 1 KB alignment)
               d.st_boff = d.tma == 2 ? 16 * 1024 : (int)rup(d.a_bytes, 1024);
               d.st_bytes = d.st_boff + (int)rup(d.bn * 128, 1024);
-              d.kg = kgroup(d.st_bytes, d.st_boff, d.kb_per_split);
-              d.nst = ring_stages(d.st_bytes, d.st_boff, d.kg);
+              d.kg = kgroup(c->pipe_bytes(), d.st_bytes, d.st_boff, d.kb_per_split);
+              d.nst = ring_stages(c->pipe_bytes(), d.st_bytes, d.st_boff, d.kg);
             } else {
               d.st_boff = 16 * 1024;
               d.st_bytes = 32 * 1024;
@@ -542,12 +557,12 @@ static mt_status plan_graphs(mt_ctx *c) {
         case MT_MAXPOOL:
         case MT_AVGPOOL:
           d.tk = TK_POOL;
-          d.pix_tile = (int)std::max<int64_t>(1, (MT_NTHREADS * MT_EW_PER_THREAD) / (os.c / 8));
+          d.pix_tile = (int)std::max<int64_t>(1, (c->nthreads() * MT_EW_PER_THREAD) / (os.c / 8));
           d.tiles = (int)cdiv((int64_t)g.batch * os.h * os.w, d.pix_tile);
           break;
         case MT_GLOBAL_AVGPOOL:
           d.tk = TK_GAP;
-          d.tiles = (int)(g.batch * cdiv(os.c / 8, 32));
+          d.tiles = (int)(g.batch * cdiv(os.c / 8, c->nthreads() / 8));
           break;
         case MT_FC:
           d.tk = TK_FC;
@@ -580,8 +595,8 @@ static mt_status plan_graphs(mt_ctx *c) {
             d.rc = d.splits > 1 ? 1 : 0;
             d.st_boff = d.a_bytes;
             d.st_bytes = d.st_boff + (int)rup(d.bn * 128, 1024);
-            d.kg = kgroup(d.st_bytes, d.st_boff, d.kb_per_split);
-            d.nst = ring_stages(d.st_bytes, d.st_boff, d.kg);
+            d.kg = kgroup(c->pipe_bytes(), d.st_bytes, d.st_boff, d.kb_per_split);
+            d.nst = ring_stages(c->pipe_bytes(), d.st_bytes, d.st_boff, d.kg);
             d.tiles = (int)(tmn * d.splits + tmn * d.rc);
             if (d.splits > 1) {
               d.cnt_off = split_cnt;
@@ -594,13 +609,13 @@ static mt_status plan_graphs(mt_ctx *c) {
             wp.bytes = (int64_t)os.c * d.K * eb;
             break;
           }
-          d.tiles = (int)(cdiv(os.c, MT_FC_ROWS) * cdiv(g.batch, MT_FC_BATCH));
+          d.tiles = (int)(cdiv(os.c, c->nthreads() / 32) * cdiv(g.batch, MT_FC_BATCH));
           wp.mode = 4;
           wp.bytes = (int64_t)os.c * d.K * eb;
           break;
         default:
           d.tk = TK_ELT;
-          d.pix_tile = (int)std::max<int64_t>(1, (MT_NTHREADS * MT_EW_PER_THREAD) / (os.c / 8));
+          d.pix_tile = (int)std::max<int64_t>(1, (c->nthreads() * MT_EW_PER_THREAD) / (os.c / 8));
           d.tiles = (int)cdiv((int64_t)g.batch * os.h * os.w, d.pix_tile);
           break;
       }
@@ -629,8 +644,8 @@ static mt_status plan_graphs(mt_ctx *c) {
         d.blk_need = d.tiles_n * (d.splits > 1 ? d.rc : 1) * (d.tma ? d.nseg : 1);
         break;
       case TK_CONV_SIMT: d.pix_blk = MT_SIMT_BM; d.blk_need = d.tiles_n; break;
-      case TK_GAP: d.pix_blk = 1; d.blk_need = (int)cdiv(d.Co / 8, 32); break;
-      case TK_FC: d.pix_blk = MT_FC_BATCH; d.blk_need = (int)cdiv(d.Co, MT_FC_ROWS); break;
+      case TK_GAP: d.pix_blk = 1; d.blk_need = (int)cdiv(d.Co / 8, c->nthreads() / 8); break;
+      case TK_FC: d.pix_blk = MT_FC_BATCH; d.blk_need = (int)cdiv(d.Co, c->nthreads() / 32); break;
       default: d.pix_blk = d.pix_tile; d.blk_need = 1; break;
     }
     d.nblk = d.blk_rows > 0 ? d.N * d.blk_tpi : (int)cdiv(npix, d.pix_blk);
@@ -797,10 +812,37 @@ static void build_stage_plan(mt_ctx *c, Schedule &s) {
       n = sm_partition(active, w, c->n_sms, &caps);
     }
     int cta = 0;
-    for (int t = 0; t < N; ++t) {
-      s.sms[k * N + t] = n[t];
-      for (int q = 0; q < n[t] && cta < c->grid; ++q) s.home[(size_t)k * c->grid + cta++] = (uint8_t)t;
+    for (int t = 0; t < N; ++t) s.sms[k * N + t] = n[t];
+    if (c->cps == 2) {
+      // f4 heterogeneous co-residency: the CTA in slot 0 of SM i serves the i-th entry of the SM
+      // partition listed from the most to the least compute-intense tenant (FLOP per byte of the
+      // stage slice), the CTA in slot 1 the list reversed -- so the two CTAs of an SM pair a
+      // compute-bound slice with a memory-bound one where the mix has both
+      std::vector<int> order;
+      for (int t = 0; t < N; ++t)
+        if (n[t] > 0) order.push_back(t);
+      std::vector<double> inten(N, 0.0);
+      for (int t : order) {
+        double F = 0.0, B = 0.0;
+        for (int j = s.ranges[(k * N + t) * 2]; j < s.ranges[(k * N + t) * 2 + 1]; ++j) {
+          F += (double)c->ops[c->T[t].op_base + j].flops;
+          B += (double)c->ops[c->T[t].op_base + j].bytes;
+        }
+        inten[t] = F / std::max(B, 1.0);
+      }
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return inten[x] > inten[y]; });
+      std::vector<int> list;
+      for (int t : order)
+        for (int q = 0; q < n[t]; ++q) list.push_back(t);
+      const int nsm = c->grid / 2;
+      for (int i = 0; i < nsm && i < (int)list.size(); ++i) {
+        s.home[(size_t)k * c->grid + i] = (uint8_t)list[i];
+        s.home[(size_t)k * c->grid + nsm + i] = (uint8_t)list[list.size() - 1 - i];
+      }
+      cta = c->grid;
     }
+    for (int t = 0; t < N && cta < c->grid; ++t)
+      for (int q = 0; q < n[t] && cta < c->grid; ++q) s.home[(size_t)k * c->grid + cta++] = (uint8_t)t;
     // grid larger than n_sms (never with 1 CTA/SM): spread the rest round-robin
     int t0 = 0;
     while (cta < c->grid) {
@@ -1048,7 +1090,7 @@ mt_status mt_set_option(mt_ctx *c, int32_t option, int64_t value) {
       if (value < 1 || value > 4096) return fail(c, MT_ERR_ARG, "bad NUM_SMS");
       if (c->loaded && value < (int64_t)c->T.size()) return fail(c, MT_ERR_ARG, "NUM_SMS < tenants");
       c->n_sms = (int)value;
-      c->grid = (int)value;
+      c->grid = (int)value * c->cps;
       if (c->has_sched) build_stage_plan(c, c->sched);
       return MT_OK;
     case MT_OPT_TIMEOUT_MS:
@@ -1056,7 +1098,24 @@ mt_status mt_set_option(mt_ctx *c, int32_t option, int64_t value) {
       c->timeout_ms = value;
       drop_graphs(c);
       return MT_OK;
-    case MT_OPT_CTAS_PER_SM: return value == 1 ? MT_OK : fail(c, MT_ERR_ARG, "only 1 CTA/SM");
+    case MT_OPT_CTAS_PER_SM: {   // f4: 2 co-resident CTAs per SM (plans depend on it: set before loading)
+      if (value != 1 && value != 2) return fail(c, MT_ERR_ARG, "CTAs per SM must be 1 or 2");
+      if (c->loaded) return fail(c, MT_ERR_STATE, "set CTAs per SM before mt_load_graphs");
+      if (!c->host_only) {
+        int bps = 0;
+        cudaError_t e = value == 2 ? mtk_cr::executor_occupancy(&bps) : mtk::executor_occupancy(&bps);
+        if (e != cudaSuccess || bps < value) {
+          char m[400], r[256] = "";
+          if (value == 2) mtk_cr::executor_resources(r, sizeof r);
+          snprintf(m, sizeof m, "executor does not fit %d CTAs per SM (occupancy %d, %s; %s)", (int)value, bps,
+                   cudaGetErrorString(e), r);
+          return fail(c, MT_ERR_REFUSED, m);
+        }
+      }
+      c->cps = (int)value;
+      c->grid = c->n_sms * c->cps;
+      return MT_OK;
+    }
     case MT_OPT_CLAIM_DEPTH:
       if (value < -(1 << 20) || value > 1 << 20) return fail(c, MT_ERR_ARG, "bad claim depth");
       if (value != 0 && c->loaded && (int)c->ops.size() > MT_GATE_OPS)
@@ -1092,6 +1151,8 @@ mt_status mt_load_graphs(mt_ctx *c, int32_t n, const mt_graph *graphs) {
     if (g.n_nodes < 1 || !g.nodes) return fail(c, MT_ERR_ARG, "empty graph");
     if (g.batch < 1 || g.in_c < 1 || g.in_h < 1 || g.in_w < 1) return fail(c, MT_ERR_ARG, "bad input shape");
     if (g.precision != MT_PREC_BF16 && g.precision != MT_PREC_FP32) return fail(c, MT_ERR_ARG, "bad precision");
+    if (c->cps == 2 && g.precision == MT_PREC_FP32)   // the fp32 SIMT conv tile assumes 256 threads
+      return fail(c, MT_ERR_REFUSED, "2 CTAs per SM: bf16 tenants only");
     c->T[t].g = g;
     c->T[t].nodes.assign(g.nodes, g.nodes + g.n_nodes);
     c->T[t].g.nodes = nullptr;
@@ -1293,7 +1354,7 @@ mt_status mt_run_async(mt_ctx *c, const float *const *inputs, float *const *outp
   if (!inputs || !outputs) return fail(c, MT_ERR_ARG, "null inputs/outputs");
   RunArgs a = base_args(c, inputs, outputs);
   if (!c->stage_split) {
-    CK(mtk::launch_executor(a, c->grid, (cudaStream_t)stream));
+    CK(k_executor(c, a, c->grid, (cudaStream_t)stream));
     return MT_OK;
   }
   // debug/profiling mode (SURVEY d.5): one launch per stage -- the kernel boundary is the stage
@@ -1309,7 +1370,7 @@ mt_status mt_run_async(mt_ctx *c, const float *const *inputs, float *const *outp
     b.no_reset = k < S - 1;
     b.ts = ts + 4 * k;
     b.ts_full = 1;
-    CK(mtk::launch_executor(b, c->grid, (cudaStream_t)stream));
+    CK(k_executor(c, b, c->grid, (cudaStream_t)stream));
   }
   return MT_OK;
 }
@@ -1359,7 +1420,7 @@ mt_status mt_run_host(mt_ctx *c, const float *const *hin, float *const *hout, fl
                          cudaMemcpyHostToDevice, s));
   }
   RunArgs a = base_args(c, din, dout);
-  CK(mtk::launch_executor(a, c->grid, s));
+  CK(k_executor(c, a, c->grid, s));
   for (int t = 0; t < N; ++t) {
     const mt_node &last = c->T[t].nodes.back();
     CK(cudaMemcpyAsync(hout[t], dout[t], (size_t)c->T[t].g.batch * last.out_c * last.out_h * last.out_w * 4,
@@ -1375,7 +1436,7 @@ mt_status mt_run_host(mt_ctx *c, const float *const *hin, float *const *hout, fl
 
 // ---- baselines: one launch per op, same tile functions (SURVEY d.2) -----------------------
 static mt_status issue_op(mt_ctx *c, const RunArgs &a, int gid, cudaStream_t s) {
-  CK(mtk::launch_op(a, c->ops[gid].d, gid, c->n_sms, s));
+  CK(k_op(c, a, c->ops[gid].d, gid, c->n_sms, s));
   return MT_OK;
 }
 
@@ -1389,7 +1450,7 @@ static mt_status issue_baseline(mt_ctx *c, int mode, const RunArgs &a, cudaStrea
   };
   if (mode == MT_BASE_SEQ || mode == MT_BASE_SEQ_GRAPH) {
     for (int t = 0; t < N; ++t)
-      if (pack_needed(t)) CK(mtk::launch_pack(a, t, main));
+      if (pack_needed(t)) CK(k_pack(c, a, t, main));
     for (int t = 0; t < N; ++t)
       for (int j = 0; j < c->T[t].L; ++j)
         if ((st = issue_op(c, a, c->T[t].op_base + j, main)) != MT_OK) return st;
@@ -1400,7 +1461,7 @@ static mt_status issue_baseline(mt_ctx *c, int mode, const RunArgs &a, cudaStrea
   for (int t = 0; t < N; ++t) CK(cudaStreamWaitEvent(c->streams[t], c->tev[0], 0));
   // packing first (a shared input is packed once; its readers wait for it)
   for (int t = 0; t < N; ++t)
-    if (pack_needed(t)) CK(mtk::launch_pack(a, t, c->streams[t]));
+    if (pack_needed(t)) CK(k_pack(c, a, t, c->streams[t]));
   std::vector<cudaEvent_t> packed_ev(N, nullptr);
   for (int t = 0; t < N; ++t) {
     int src = t;
@@ -1536,7 +1597,7 @@ static mt_status profile_impl(mt_ctx *c, int32_t n, const std::vector<Schedule> 
         a.ts_full = 0;
         for (int r = 0; r < runs; ++r, ++slot) {
           a.ts = (unsigned long long *)(c->ws + c->lay.prof_ts + slot * 16);
-          CK(mtk::launch_executor(a, c->grid, s));
+          CK(k_executor(c, a, c->grid, s));
         }
       }
       std::vector<unsigned long long> ts(slot * 2);

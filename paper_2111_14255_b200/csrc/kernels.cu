@@ -14,11 +14,12 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include "kernels.h"
 #include "mt_types.h"
 
-namespace mtk {
+namespace MT_NS {
 
 typedef __nv_bfloat16 bf16;
 
@@ -34,6 +35,7 @@ struct CtaShared {
   unsigned long long bar_accf;
   uint32_t tmem_base;
   int op, tile, last, ok, home, ten;
+  int vcta;                   // index into the home table: blockIdx.x, or (2 CTAs/SM) slot * #SMs + SM
   int smem_cap;               // bytes of dynamic shared memory this kernel has (staging budget)
   int tracing;                // mt_set_trace on: extra producer stamps
   unsigned long long t_pick, t_pick_next, t_deps, t_mma, t_run, t_first, t_lastmma, t_aissue;
@@ -473,7 +475,7 @@ __device__ void conv_tc_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaSh
       if (i < ct.nk) {
         const int kb = ct.kb0 + i;
         const uint32_t sb = s0 + i * d.st_bytes + d.st_boff;
-        for (int row = tid >> 3; row < d.bn; row += 32) {
+        for (int row = tid >> 3; row < d.bn; row += MT_NTHREADS / 8) {
           const bf16 *src = Wt + (int64_t)(ct.n0 + row) * d.Kpad + kb * MT_BK + c * 8;
           cp_async16(sb + row * 128 + ((c ^ (row & 7)) << 4), src, true);
         }
@@ -489,16 +491,17 @@ __device__ void conv_tc_prefetch(const OpDesc &d, int tile, uint8_t *smem, CtaSh
     }
     return;
   }
-  if (tid < d.bn) {
-    const int n = ct.n0 + tid;
-    sh.esc[tid] = n < d.Co ? __ldg(reinterpret_cast<const float *>(d.scale) + n) : 0.f;
-    sh.esh[tid] = n < d.Co ? __ldg(reinterpret_cast<const float *>(d.shift) + n) : 0.f;
+  for (int c = tid; c < d.bn; c += MT_NTHREADS) {   // bn may exceed the CTA (2 CTAs/SM: 128 threads)
+    const int n = ct.n0 + c;
+    sh.esc[c] = n < d.Co ? __ldg(reinterpret_cast<const float *>(d.scale) + n) : 0.f;
+    sh.esh[c] = n < d.Co ? __ldg(reinterpret_cast<const float *>(d.shift) + n) : 0.f;
   }
   // the rest of this split's weight rows -> L2 (one bulk prefetch per row)
   const int kpre = d.tma ? d.nst * d.kg : MT_STAGES;   // k-blocks whose weights are already requested
-  if (ct.nk > kpre && tid < d.bn)
-    prefetch_l2_bulk(Wt + (int64_t)(ct.n0 + tid) * d.Kpad + (ct.kb0 + kpre) * MT_BK,
-                     (uint32_t)(ct.nk - kpre) * MT_BK * 2);
+  if (ct.nk > kpre)
+    for (int row = tid; row < d.bn; row += MT_NTHREADS)
+      prefetch_l2_bulk(Wt + (int64_t)(ct.n0 + row) * d.Kpad + (ct.kb0 + kpre) * MT_BK,
+                       (uint32_t)(ct.nk - kpre) * MT_BK * 2);
 }
 
 __device__ __forceinline__ bool elect_one() {
@@ -650,11 +653,12 @@ __device__ __forceinline__ void conv_tc_mainloop_cpasync(const RunArgs &a, const
   const bf16 *Wt = reinterpret_cast<const bf16 *>(d.w);
   const int HoWo = d.Ho * d.Wo;
   const int c = tid & 7;
-  int pbase[4], hb[4], wb[4];
-  bool rv[4];
+  constexpr int RP = MT_NTHREADS / 8, NP = MT_BM / RP;   // rows per pass, passes per tile
+  int pbase[NP], hb[NP], wb[NP];
+  bool rv[NP];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = m0 + (tid >> 3) + 32 * i;
+  for (int i = 0; i < NP; ++i) {
+    const int m = m0 + (tid >> 3) + RP * i;
     rv[i] = m < d.M;
     const int mm = rv[i] ? m : 0;
     const int n = mm / HoWo, rem = mm - n * HoWo;
@@ -680,8 +684,8 @@ __device__ __forceinline__ void conv_tc_mainloop_cpasync(const RunArgs &a, const
       const int rr = tap / d.kw, ss = tap - rr * d.kw;
       const uint32_t sa = s0 + s * d.st_bytes;
 #pragma unroll
-      for (int i2 = 0; i2 < 4; ++i2) {
-        const int row = (tid >> 3) + 32 * i2;
+      for (int i2 = 0; i2 < NP; ++i2) {
+        const int row = (tid >> 3) + RP * i2;
         const int hi = hb[i2] + rr, wi = wb[i2] + ss;
         const bool valid = kv && rv[i2] && hi >= 0 && hi < d.H && wi >= 0 && wi < d.W;
         const bf16 *src = valid ? X + (int64_t)(pbase[i2] + hi * d.W + wi) * d.in_cs + d.in_co + ci : X;
@@ -689,7 +693,7 @@ __device__ __forceinline__ void conv_tc_mainloop_cpasync(const RunArgs &a, const
       }
       if (jj > 0) {
         const uint32_t sb = sa + d.st_boff;
-        for (int row = tid >> 3; row < d.bn; row += 32) {
+        for (int row = tid >> 3; row < d.bn; row += RP) {
           const bf16 *src = Wt + (int64_t)(n0 + row) * d.Kpad + kb * MT_BK + c * 8;
           cp_async16(sb + row * 128 + ((c ^ (row & 7)) << 4), src, true);
         }
@@ -876,12 +880,12 @@ __device__ void conv_tc_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_
 
   // epilogue: warp w drains TMEM lanes 32*(w&3).. and column half (w>>2)
   const int warp = tid >> 5, lane = tid & 31;
-  const int q = warp & 3, half = warp >> 2;
+  const int q = warp & 3, half = warp >> 2;   // 2 CTAs/SM: 4 warps, each drains all columns
   const int r = 32 * q + lane;
   const int m = conv_row_pixel(d, ct, r);
-  const int hcols = d.bn >> 1;
+  const int hcols = d.bn / (MT_NTHREADS / 128);
   const uint32_t tl = sh.tmem_base + ((uint32_t)(32 * q) << 16);
-  const bool stamp = a.trace != nullptr && (tid == 0 || tid == 255);
+  const bool stamp = a.trace != nullptr && (tid == 0 || tid == MT_NTHREADS - 1);
   if (stamp) sh.t_kb[tid == 0 ? 0 : 2] = gtimer();   // epilogue start (warp 0 / warp 7)
   if (S == 1) {
     if (hcols >= 32) {
@@ -1372,8 +1376,8 @@ template <typename T>
 __device__ void gap_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_t *smem) {
   const T *X = in_ptr<T>(a, d);
   const int cg = d.C >> 3;
-  const int tiles_c = (cg + 31) >> 5;
-  const int n = tile / tiles_c, g0 = (tile - n * tiles_c) * 32;
+  const int tiles_c = (cg + MT_GAP_G - 1) / MT_GAP_G;
+  const int n = tile / tiles_c, g0 = (tile - n * tiles_c) * MT_GAP_G;
   const int g = g0 + (threadIdx.x >> 3), lane = threadIdx.x & 7;
   const int HW = d.H * d.W;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1396,7 +1400,7 @@ __device__ void gap_tile(const RunArgs &a, const OpDesc &d, int tile, uint8_t *s
       for (int q = 0; q < 8; ++q) acc[q] += x[q];
     }
   }
-  float *red = reinterpret_cast<float *>(smem);   // [256][8]
+  float *red = reinterpret_cast<float *>(smem);   // [MT_NTHREADS][8]
 #pragma unroll
   for (int q = 0; q < 8; ++q) red[threadIdx.x * 8 + q] = acc[q];
   __syncthreads();
@@ -1601,7 +1605,7 @@ __device__ __forceinline__ void tile_out_range(const OpDesc &d, int tile, int64_
       }
       break;
     case TK_CONV_SIMT: p0 = (int64_t)(tile / d.tiles_n) * MT_SIMT_BM; p1 = p0 + MT_SIMT_BM; break;
-    case TK_GAP: p0 = tile / ((d.Co / 8 + 31) / 32); p1 = p0 + 1; break;
+    case TK_GAP: p0 = tile / ((d.Co / 8 + MT_GAP_G - 1) / MT_GAP_G); p1 = p0 + 1; break;
     case TK_FC: p0 = (int64_t)(tile / ((d.Co + MT_FC_ROWS - 1) / MT_FC_ROWS)) * MT_FC_BATCH; p1 = p0 + MT_FC_BATCH; break;
     default: p0 = (int64_t)tile * d.pix_tile; p1 = p0 + d.pix_tile; break;
   }
@@ -1636,7 +1640,7 @@ __device__ __forceinline__ int tile_block(const OpDesc &d, int tile, const CtaSh
       return tile >= nct ? ((tile - nct) / d.rc) / d.tiles_n / ns : -1;   // only reduce tiles complete
     }
     case TK_CONV_SIMT: return tile / d.tiles_n;
-    case TK_GAP: return tile / ((d.Co / 8 + 31) / 32);
+    case TK_GAP: return tile / ((d.Co / 8 + MT_GAP_G - 1) / MT_GAP_G);
     case TK_FC: return tile / ((d.Co + MT_FC_ROWS - 1) / MT_FC_ROWS);
     default: return tile;
   }
@@ -1798,7 +1802,7 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
       sh.beg[t] = sh.cur[t] = a.rng[(s * T + t) * 2];
       sh.end[t] = a.rng[(s * T + t) * 2 + 1];
     }
-    sh.home = a.home[(size_t)s * gridDim.x + blockIdx.x];
+    sh.home = a.home[(size_t)s * gridDim.x + sh.vcta];
   }
   __syncthreads();
   while (true) {
@@ -1968,13 +1972,32 @@ __device__ bool run_stage(const RunArgs &a, int s, uint8_t *smem, CtaShared &sh,
   }
 }
 
+__device__ __forceinline__ uint32_t sm_id() {
+  uint32_t v;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(v));
+  return v;
+}
+
 template <bool F32>
-__global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
+__global__ void __launch_bounds__(MT_NTHREADS, MT_PIPE_BYTES_1 / MT_PIPE_BYTES) executor_kernel(RunArgs a) {
   uint8_t *smem = smem_base();
   __shared__ __align__(16) CtaShared sh;
   PipeState ps{0u, 0u, 0u};
   if (threadIdx.x < 64) sh.complete[threadIdx.x] = 0u;
-  if (threadIdx.x == 0) { sh.smem_cap = PIPE_BYTES; sh.tracing = a.trace != nullptr; }
+  if (threadIdx.x == 0) {
+    sh.smem_cap = PIPE_BYTES;
+    sh.tracing = a.trace != nullptr;
+    sh.vcta = blockIdx.x;
+#ifdef MT_CR
+    // f4 co-residency: the home table is laid out per (slot, SM) so the host can pair tenants of
+    // different kinds on one SM; the slot is this CTA's arrival order on its SM
+    const uint32_t sm = sm_id();
+    const int nsm = gridDim.x / 2;
+    const int slot = sm < 256 ? atomicAdd(&a.ctl->smslot[sm], 1) : 2;
+    if (slot < 2 && (int)sm < nsm) sh.vcta = slot * nsm + (int)sm;
+    else atomicExch(&a.ctl->error, 4u);   // SM ids outside [0, #SMs): no (slot, SM) home layout
+#endif
+  }
   if (a.claim_depth != 0)
     for (int i = threadIdx.x; i < a.n_ops; i += blockDim.x) sh.gate[i] = (int16_t)__ldg(a.gates + i);
   cta_setup(sh, true);
@@ -2011,6 +2034,12 @@ __global__ void __launch_bounds__(MT_NTHREADS, 1) executor_kernel(RunArgs a) {
       a.blkcnt[i] = 0;
     if (blockIdx.x == 0 && threadIdx.x < MT_MAXT) a.ctl->gcur[threadIdx.x] = 0;
   }
+#ifdef MT_CR
+  if (threadIdx.x == 0) {
+    const uint32_t sm = sm_id();
+    if (sm < 256) atomicSub(&a.ctl->smslot[sm], 1);
+  }
+#endif
   cta_teardown(sh, true);
 }
 
@@ -2131,10 +2160,14 @@ size_t executor_smem_bytes() { return SMEM_BYTES; }
 static cudaError_t set_attrs() {
   static bool done = false;
   if (done) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(executor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(executor_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  if (e != cudaSuccess) return e;
+  for (auto f : {executor_kernel<true>, executor_kernel<false>}) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    // the whole unified L1/shared array as shared memory (2 CTAs/SM need 2 x ~107 KB)
+    e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e;
   for (auto f : {op_kernel<true>, op_kernel<false>}) {
     e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
@@ -2150,7 +2183,45 @@ static cudaError_t set_attrs() {
 cudaError_t executor_occupancy(int *bps) {
   cudaError_t e = set_attrs();
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, executor_kernel<true>, MT_NTHREADS, SMEM_BYTES);
+#ifdef MT_CR
+  // the runtime's occupancy calculator reports 1 CTA/SM for every kernel containing tcgen05
+  // instructions (tools/occ_probe.cu: even a 4-register kernel), while the hardware runs two per
+  // SM (same probe: 296 CTAs allocating TMEM, 148 same-SM pairs overlapping).  Count the resources
+  // instead: registers (allocated per thread in multiples of 8) and shared memory.
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, executor_kernel<false>);
+  if (e != cudaSuccess) return e;
+  int dev = 0, smem_sm = 0, regs_sm = 0, resv = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+  const int by_regs = regs_sm / (((fa.numRegs + 7) / 8 * 8) * MT_NTHREADS);
+  const int by_smem = smem_sm / ((int)fa.sharedSizeBytes + SMEM_BYTES + resv);
+  *bps = by_regs < by_smem ? by_regs : by_smem;
+  return cudaSuccess;
+#else
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, executor_kernel<false>, MT_NTHREADS, SMEM_BYTES);
+#endif
+}
+
+// resource summary of the bf16 executor (diagnostics of the co-residency check)
+int executor_resources(char *buf, int n) {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, executor_kernel<false>) != cudaSuccess) return 0;
+  int dev = 0, smem_sm = 0, regs_sm = 0, smem_blk = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&smem_blk, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+  int o1 = -1, o2 = -1, o3 = -1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, executor_kernel<false>, MT_NTHREADS, 80 * 1024);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, executor_kernel<false>, MT_NTHREADS, 32 * 1024);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, executor_kernel<false>, MT_NTHREADS, 0);
+  return snprintf(buf, n, "regs %d static smem %zu dyn %d (max dyn %d) local %zu; SM: smem %d regs %d reserved/blk %d; "
+                  "occ at 80K/32K/0 dyn: %d %d %d",
+                  fa.numRegs, fa.sharedSizeBytes, SMEM_BYTES, fa.maxDynamicSharedSizeBytes, fa.localSizeBytes, smem_sm,
+                  regs_sm, smem_blk, o1, o2, o3);
 }
 
 cudaError_t launch_executor(const RunArgs &a, int grid, cudaStream_t s) {
@@ -2159,8 +2230,19 @@ cudaError_t launch_executor(const RunArgs &a, int grid, cudaStream_t s) {
   void *args[] = {(void *)&a};
   bool f32 = false;
   for (int t = 0; t < a.n_tenants; ++t) f32 |= a.in_prec[t] == 1;
+#ifdef MT_CR
+  // 2 CTAs/SM: cudaLaunchCooperativeKernel applies the calculator's 1-CTA/SM limit to tcgen05 kernels
+  // (see executor_occupancy), so this build launches normally; the grid fits the GPU by the resource
+  // count, and a CTA that could not become resident would end the run by the grid-barrier timeout
+  // (MT_ERR_INTERNAL), never hang it
+  (void)args;
+  if (f32) executor_kernel<true><<<grid, MT_NTHREADS, SMEM_BYTES, s>>>(a);
+  else executor_kernel<false><<<grid, MT_NTHREADS, SMEM_BYTES, s>>>(a);
+  return cudaGetLastError();
+#else
   return cudaLaunchCooperativeKernel(f32 ? (void *)executor_kernel<true> : (void *)executor_kernel<false>,
                                      dim3(grid), dim3(MT_NTHREADS), args, SMEM_BYTES, s);
+#endif
 }
 
 cudaError_t launch_op(const RunArgs &a, const OpDesc &d, int op, int max_grid, cudaStream_t s) {
@@ -2198,4 +2280,4 @@ cudaError_t launch_weight_pack(int mode, const float *src, void *dst, const OpDe
   return cudaGetLastError();
 }
 
-}  // namespace mtk
+}  // namespace MT_NS

@@ -6,17 +6,33 @@
 #define MT_MAXT 16        // max tenants (== MT_MAX_TENANTS)
 #define MT_MAXIN 8        // max inputs of one op (== MT_MAX_INPUTS)
 #define MT_MAXDEP 9       // inputs + residual
-#define MT_NTHREADS 256   // threads per CTA of every kernel
+// Device-code configuration.  kernels.cu is compiled twice:
+//  * default: one 256-thread CTA per SM with a 192 KB conv ring (namespace mtk);
+//  * MT_CR (kernels_cr.cu, MT_OPT_CTAS_PER_SM = 2): two co-resident 128-thread CTAs per SM, each
+//    with a 96 KB ring, 255 registers per thread (2 x 128 x 256 = the whole register file) and 256
+//    TMEM columns (namespace mtk_cr).
+// The host plans with the values of the configuration the context runs (mt_ctx::dev).
+#ifdef MT_CR
+#define MT_NTHREADS 128   // threads per CTA of every kernel
+#define MT_PIPE_BYTES (96 * 1024)    // shared-memory ring of the conv pipeline
+#define MT_NS mtk_cr
+#else
+#define MT_NTHREADS 256
+#define MT_PIPE_BYTES (192 * 1024)
+#define MT_NS mtk
+#endif
+#define MT_PIPE_BYTES_1 (192 * 1024)   // ring of the 1-CTA-per-SM configuration (host planning)
+#define MT_PIPE_BYTES_2 (96 * 1024)    // ring of the 2-CTA-per-SM configuration
 #define MT_STAGES 4       // smem pipeline depth of the cp.async conv mainloop (32 KB stages)
 #define MT_MAXST 12       // max pipeline depth of the TMA conv mainloop (stage = A box + B box)
-#define MT_PIPE_BYTES (192 * 1024)   // shared-memory ring of the conv pipeline
 #define MT_BM 128         // tcgen05 conv tile rows (output pixels), UMMA M
 #define MT_BK 64          // K per pipeline stage (one 128-byte swizzle atom of bf16)
 #define MT_SIMT_BM 64     // SIMT conv tile
 #define MT_SIMT_BN 64
 #define MT_SIMT_BK 16
 #define MT_EW_PER_THREAD 2   // 8-channel vectors per thread in pointwise tiles
-#define MT_FC_ROWS 8         // FC output rows per tile (one per warp)
+#define MT_FC_ROWS (MT_NTHREADS / 32)   // FC output rows per tile (one per warp)
+#define MT_GAP_G (MT_NTHREADS / 8)      // GAP: 8-channel groups per tile (8 threads each)
 #define MT_FC_BATCH 8        // FC batch columns per pass
 #define MT_GATE_OPS 2048     // bounded claim-ahead: gate table staged in shared memory (ops)
 
@@ -82,6 +98,7 @@ struct CtlBlock {
   unsigned int trace_count;  // entries written to the trace buffer
   unsigned long long err_info;
   int gcur[MT_MAXT];         // per tenant: every op below is fully claimed (monotonic hint; reset per run)
+  int smslot[256];           // 2 CTAs/SM: CTAs resident on SM i so far (slot counter; back to 0 at exit)
 };
 
 struct RunArgs {

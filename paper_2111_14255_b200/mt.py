@@ -25,6 +25,7 @@ MT_OK, MT_ERR_INTERNAL, MT_ERR_VALIDATION, MT_ERR_REFUSED, MT_ERR_CUDA, MT_ERR_A
 MT_MAX_INPUTS = 8
 MT_MAX_TENANTS = 16
 MT_OPT_STEAL, MT_OPT_NUM_SMS, MT_OPT_TIMEOUT_MS, MT_OPT_PARTITION, MT_OPT_CLAIM_DEPTH, MT_OPT_STAGE_SPLIT = 1, 2, 3, 5, 6, 7
+MT_OPT_CTAS_PER_SM = 4
 BASE_MODES = {"seq": 1, "ms_dfs": 2, "ms_bfs": 3, "seq_graph": 4, "ms_graph": 5, "stage_events": 6}
 
 

@@ -13,10 +13,12 @@ from .mt import Context
 class TenantMix:
     """N tenant graphs loaded into one mt_ctx on a CUDA device, weights resident in HBM."""
 
-    def __init__(self, graphs, device=0, steal=True):
+    def __init__(self, graphs, device=0, steal=True, ctas_per_sm=1):
         self.graphs = graphs
         self.dev = torch.device("cuda", device)
         self.ctx = Context(device)
+        if ctas_per_sm != 1:   # f4 co-residency build (MT_OPT_CTAS_PER_SM; before loading)
+            self.ctx.set_option(4, int(ctas_per_sm))
         if steal is not True:
             self.ctx.set_option(1, int(steal))
         self._params = []

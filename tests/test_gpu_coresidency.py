@@ -1,0 +1,100 @@
+"""heterogeneous co-residency (MT_OPT_CTAS_PER_SM = 2): two 128-thread executor
+CTAs per SM (kernels_cr.cu), the SM's two slots serving a compute-bound and a memory-bound slice
+(P:161-166).  Every op against the oracle, and the outputs bit-identical to the 1-CTA-per-SM
+executor's: co-residency changes where and when tiles run, never what they compute.
+Run: pytest -m gpu."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from workloads import configs, zoo  # noqa: E402
+
+from .gpu_helpers import teacher_forced_errors  # noqa: E402
+
+_MIXES = {}
+
+
+def mix(config, cps):
+    key = (config, cps)
+    if key not in _MIXES:
+        from paper_2111_14255_b200.session import TenantMix
+        graphs = configs.tenants(config)
+        m = TenantMix(graphs, ctas_per_sm=cps)
+        x = zoo.make_input(graphs[0])
+        m.set_input(x)
+        m.x_np = x
+        _MIXES[key] = m
+    return _MIXES[key]
+
+
+def _outs(m):
+    torch.cuda.synchronize()
+    return [o.clone() for o in m.outputs]
+
+
+@pytest.mark.parametrize("config", ["c2", "c3", "c4", "c4b8"])
+def test_coresident_teacher_forced_every_op(config):
+    m = mix(config, 2)
+    L = [g.n_ops for g in m.graphs]
+    m.ctx.set_schedule_pointers(configs.all_concurrent_pointers(L))
+    m.run()
+    for t, g in enumerate(m.graphs):
+        errs = teacher_forced_errors(m, m.x_np, t)
+        worst = int(np.argmax(errs))
+        assert max(errs) <= 1e-2, (g.name, worst, g.nodes[worst]["kind"], errs[worst])
+
+
+@pytest.mark.parametrize("config", ["c2", "c4", "c4b8"])
+def test_coresident_same_bits_as_one_cta_per_sm(config):
+    """same tile shapes and split-K factors (the plan's cost model does not depend on the ring
+    size), the same UMMA order and reductions -> the same bits, under every schedule tried and the
+    per-op-launch baselines of the co-resident build"""
+    m1, m2 = mix(config, 1), mix(config, 2)
+    L = [g.n_ops for g in m1.graphs]
+    m1.ctx.set_schedule_pointers(configs.all_concurrent_pointers(L))
+    m1.run()
+    ref = _outs(m1)
+    cands = [configs.all_concurrent_pointers(L), configs.sequential_pointers(L), configs.uniform_pointers(L)] + \
+        configs.sample_candidates(L, 40, seed=11)[2:]
+    n_ok = 0
+    for rho in cands:
+        try:
+            m2.ctx.set_schedule_pointers(rho)
+        except Exception:
+            continue
+        n_ok += 1
+        for o in m2.outputs:
+            o.fill_(float("nan"))
+        m2.ctx.run_async(m2.in_ptrs, m2.out_ptrs)
+        for a, b in zip(_outs(m2), ref):
+            assert torch.equal(a, b), rho
+    assert n_ok >= 30
+    m2.ctx.set_schedule_pointers(configs.uniform_pointers(L))
+    for mode in ("seq", "ms_bfs", "stage_events"):
+        for o in m2.outputs:
+            o.fill_(float("nan"))
+        m2.ctx.run_baseline(mode, m2.in_ptrs, m2.out_ptrs)
+        for a, b in zip(_outs(m2), ref):
+            assert torch.equal(a, b), mode
+
+
+def test_coresident_knobs_and_steal_off():
+    """strict partition (no stealing: each tenant only on its own (slot, SM) homes) and the
+    latency-balanced rule with bounded claim-ahead still complete with the same bits"""
+    m1, m2 = mix("c3", 1), mix("c3", 2)
+    L = [g.n_ops for g in m1.graphs]
+    m1.ctx.set_schedule_pointers(configs.all_concurrent_pointers(L))
+    m1.run()
+    ref = _outs(m1)
+    m2.ctx.set_schedule_pointers(configs.uniform_pointers(L))
+    for knobs in ((1, 2, 2), (0, 0, 0), (1, 0, 1)):
+        m2.set_knobs(knobs)
+        for o in m2.outputs:
+            o.fill_(float("nan"))
+        m2.run()
+        for a, b in zip(_outs(m2), ref):
+            assert torch.equal(a, b), knobs
+    m2.set_knobs((0, 0, 2))

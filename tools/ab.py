@@ -1,7 +1,7 @@
 """Same-box A/B timing of alternative builds of libmt.so (box-to-box variance is ~5%, larger than
 most single changes).  Variants are prebuilt .so files; runs alternate variants per config.
 
-  python tools/ab.py --libs ab/A.so,ab/B.so --configs c2,c3 --rounds 3 --runs 20
+  python tools/ab.py --libs ab/A.so,ab/B.so,ab/B.so@2 --configs c2,c3 --rounds 3 --runs 20   (@2: 2 CTAs/SM)
 """
 import argparse
 import os
@@ -23,10 +23,12 @@ res = {}
 for r in range(a.rounds):
     for cfg in a.configs.split(","):
         for lib in (libs if r % 2 == 0 else libs[::-1]):
-            env = dict(os.environ, MT_LIB_PATH=os.path.abspath(lib))
+            path, _, cps = lib.partition("@")   # "lib.so@2": run with 2 executor CTAs per SM
+            env = dict(os.environ, MT_LIB_PATH=os.path.abspath(path))
             kn = dict(x.split("=") for x in a.knobs.split(";")) if "=" in a.knobs else {}
             out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "prof_exec.py"), "--config", cfg,
-                                  "--runs", str(a.runs), "--knobs", kn.get(cfg, a.knobs if not kn else "0,0")],
+                                  "--runs", str(a.runs), "--knobs", kn.get(cfg, a.knobs if not kn else "0,0"),
+                                  "--cps", cps or "1"],
                                  capture_output=True, text=True, env=env, timeout=300).stdout
             us = [float(m) for m in re.findall(r"run \d+: ([0-9.]+) us", out)][3:]
             res.setdefault((cfg, lib), []).extend(us)

@@ -9,5 +9,5 @@ else git -C $ROOT archive $REV paper_2111_14255_b200/csrc include | tar -x -C $T
 S=$TMP/paper_2111_14255_b200/csrc
 mkdir -p $(dirname $ROOT/$OUT)
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 -shared \
-  --expt-relaxed-constexpr $NVFLAGS -o $ROOT/$OUT $S/kernels.cu $S/host.cpp $S/plan.cpp -ldl -lpthread -lrt
+  --expt-relaxed-constexpr $NVFLAGS -o $ROOT/$OUT $S/kernels.cu $S/kernels_cr.cu $S/host.cpp $S/plan.cpp -ldl -lpthread -lrt
 rm -rf $TMP

@@ -21,10 +21,11 @@ ap.add_argument("--baseline", default=None)
 ap.add_argument("--steal", type=int, default=2)
 ap.add_argument("--knobs", default="0,0", help="partition rule, claim depth (TenantMix.calibrate)")
 ap.add_argument("--stage-split", action="store_true", help="one executor launch per stage (ncu per stage)")
+ap.add_argument("--cps", type=int, default=1, help="executor CTAs per SM (2: f4 co-residency build)")
 a = ap.parse_args()
 g = configs.tenants(a.config)
 L = [x.n_ops for x in g]
-m = TenantMix(g, steal=a.steal)
+m = TenantMix(g, steal=a.steal, ctas_per_sm=a.cps)
 m.set_input(zoo.make_input(g[0]))
 rho = {"all_concurrent": configs.all_concurrent_pointers, "sequential": configs.sequential_pointers,
        "uniform4": configs.uniform_pointers}[a.schedule](L)
