@@ -210,6 +210,11 @@ mt_status mt_stage_assignment(mt_ctx *ctx, int32_t *stage_of);
 /* sms[S][N]: CTAs whose home queue is tenant i in stage s (runtime-aware partition, a3;
  * rule chosen by MT_OPT_PARTITION; every active tenant >= 1, inactive 0, sum = #SMs) */
 mt_status mt_sm_partition(mt_ctx *ctx, int32_t *sms);
+/* *grid = executor CTAs per launch (#SMs x MT_OPT_CTAS_PER_SM); homes[S][grid] (may be NULL to
+ * query the grid): the home tenant of every CTA per stage.  1 CTA/SM: CTA index; 2 CTAs/SM: index
+ * slot * #SMs + SM id, slot 0 listing the partition from the most to the least compute-intense
+ * tenant (FLOP/byte of the stage slice), slot 1 the same list reversed (f4 pairing). */
+mt_status mt_stage_homes(mt_ctx *ctx, int32_t *grid, int32_t *homes);
 
 /* Run the active schedule once on the persistent stage executor (one cooperative launch).
  * inputs[N]: DEVICE fp32 NCHW graph inputs (may alias: the shared input of P:240).

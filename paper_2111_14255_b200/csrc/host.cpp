@@ -43,6 +43,9 @@ static constexpr int BN_MIN = 32;        // narrowest N tile the cost model cons
 // The UMMA reads all 128 rows (16 KB) of an A sub-block even when the box holds fewer output
 // pixels (e.g. 25 at 5x5): the rows past the box are discarded by the epilogue, but the read must
 // stay inside the ring, so the last sub-block needs (16 KB - A region) bytes of slack behind it.
+#ifndef MT_CR_PAIR
+#define MT_CR_PAIR 1   // 2 CTAs/SM: slot 1 lists the partition reversed (0: same order, ablation)
+#endif
 #ifndef MT_KB_OVH
 #define MT_KB_OVH 0.0   // cost model: us of issue-chain latency per ring stage (divided over its kg k-blocks)
 #endif
@@ -837,7 +840,7 @@ static void build_stage_plan(mt_ctx *c, Schedule &s) {
       const int nsm = c->grid / 2;
       for (int i = 0; i < nsm && i < (int)list.size(); ++i) {
         s.home[(size_t)k * c->grid + i] = (uint8_t)list[i];
-        s.home[(size_t)k * c->grid + nsm + i] = (uint8_t)list[list.size() - 1 - i];
+        s.home[(size_t)k * c->grid + nsm + i] = (uint8_t)list[MT_CR_PAIR ? list.size() - 1 - i : i];
       }
       cta = c->grid;
     }
@@ -1345,6 +1348,15 @@ mt_status mt_sm_partition(mt_ctx *c, int32_t *sms) {
   if (!c || !sms) return MT_ERR_ARG;
   if (!c->has_sched) return fail(c, MT_ERR_STATE, "no schedule set");
   memcpy(sms, c->sched.sms.data(), c->sched.sms.size() * 4);
+  return MT_OK;
+}
+
+mt_status mt_stage_homes(mt_ctx *c, int32_t *grid, int32_t *homes) {
+  if (!c || !grid) return MT_ERR_ARG;
+  *grid = c->grid;
+  if (!homes) return MT_OK;
+  if (!c->has_sched) return fail(c, MT_ERR_STATE, "no schedule set");
+  for (size_t i = 0; i < c->sched.home.size(); ++i) homes[i] = c->sched.home[i];
   return MT_OK;
 }
 

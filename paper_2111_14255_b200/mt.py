@@ -77,6 +77,7 @@ _sig = {
     "mt_get_schedule": (C.c_int, [P, I32P]),
     "mt_stage_assignment": (C.c_int, [P, I32P]),
     "mt_sm_partition": (C.c_int, [P, I32P]),
+    "mt_stage_homes": (C.c_int, [P, I32P, I32P]),
     "mt_run": (C.c_int, [P, C.POINTER(P), C.POINTER(P), F32P, F32P, P]),
     "mt_run_async": (C.c_int, [P, C.POINTER(P), C.POINTER(P), P]),
     "mt_run_host": (C.c_int, [P, C.POINTER(P), C.POINTER(P), F32P, P]),
@@ -257,6 +258,14 @@ class Context:
         S = self.num_stages()
         out = np.zeros((S, self.n_tenants), np.int32)
         self.check(mt_sm_partition(self.h, out.ctypes.data_as(I32P)))
+        return out
+
+    def stage_homes(self):
+        """[S][grid] home tenant of every executor CTA per stage (mt_stage_homes)"""
+        g = C.c_int32(0)
+        self.check(mt_stage_homes(self.h, C.byref(g), None))
+        out = np.zeros((self.num_stages(), g.value), np.int32)
+        self.check(mt_stage_homes(self.h, C.byref(g), out.ctypes.data_as(I32P)))
         return out
 
     # ---- execution ---------------------------------------------------------------------
