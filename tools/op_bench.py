@@ -25,13 +25,14 @@ ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--groups", type=int, default=1)
 ap.add_argument("--runs", type=int, default=20)
 ap.add_argument("--internal", type=int, default=1)
+ap.add_argument("--cps", type=int, default=1, help="executor CTAs per SM (2: f4 co-resident build)")
 a = ap.parse_args()
 b = zoo.GraphBuilder("tinyA", a.batch, a.cin, a.hw, a.hw, zoo.PREC_BF16, seed=0)
 x = b.relu(-1) if a.internal else -1    # internal input: the conv takes the TMA operand path
 x = b.conv(x, a.cout, a.k, a.s, a.p, groups=a.groups)
 b.gap(x)
 g = b.build()
-m = TenantMix([g])
+m = TenantMix([g], ctas_per_sm=a.cps)
 m.set_input(zoo.make_input(g))
 m.ctx.set_schedule_pointers([[]])
 ci = 1 if a.internal else 0
