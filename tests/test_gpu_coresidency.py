@@ -98,3 +98,26 @@ def test_coresident_knobs_and_steal_off():
         for a, b in zip(_outs(m2), ref):
             assert torch.equal(a, b), knobs
     m2.set_knobs((0, 0, 2))
+
+
+def test_coresident_profile_batch_and_host_run():
+    """the profiling entry point (a10) and the host-buffer run in the co-resident configuration:
+    statuses from the IR, finite latencies, and mt_run_host = the device run bit for bit"""
+    from oracle import ir
+    m = mix("c2", 2)
+    L = [g.n_ops for g in m.graphs]
+    cands = configs.sample_candidates(L, 16, seed=5)
+    cands.append([[0, 0], [0, 0]])          # all-empty stages -> infeasible
+    lat, st = m.ctx.profile_batch_pointers(cands, m.in_ptrs, m.out_ptrs, warmup=1, iters=3)
+    for k, rho in enumerate(cands):
+        ok = ir.T(L, rho)[0][0] == ir.E_OK
+        assert (st[k] == 0) == ok
+        assert (1.0 < lat[k] < 1e5) if ok else np.isnan(lat[k])
+    m.ctx.set_schedule_pointers(configs.uniform_pointers(L))
+    m.run()
+    ref = _outs(m)
+    xh = torch.from_numpy(m.x_np).pin_memory()
+    outs_h = [torch.empty(o.shape, dtype=torch.float32).pin_memory() for o in m.outputs]
+    m.ctx.run_host([xh.data_ptr()] * len(L), [o.data_ptr() for o in outs_h])
+    for a, b in zip(outs_h, ref):
+        assert torch.equal(a, b.cpu())

@@ -64,13 +64,29 @@ def main():
         t0 = time.time()
         g = configs.tenants(cfg)
         L = [x.n_ops for x in g]
-        m = TenantMix(g)
-        m.set_input(zoo.make_input(g[0]))
+        r = {"tenants": list(configs.CONFIGS[cfg][0]), "ops": L}
+        # executor configuration (1 or 2 CTAs per SM, f4) and knobs (partition rule, claim depth,
+        # steal) chosen by measurement, as in bench.py
+        cal = {}
+        for cps in ((1, 2) if not a.no_calibrate else (1,)):
+            try:
+                mm = TenantMix(g, ctas_per_sm=cps)
+            except Exception:
+                continue
+            mm.set_input(zoo.make_input(g[0]))
+            if a.no_calibrate:
+                cal[cps] = (mm, None, None, 0.0)
+                continue
+            kn, med = mm.calibrate()
+            cal[cps] = (mm, kn, med, med[kn])
+        cps = min(cal, key=lambda c: cal[c][3])
+        m, kn, med, _ = cal[cps]
+        r["ctas_per_sm"] = cps
+        r["calibration_us_by_ctas_per_sm"] = {c: round(v[3], 1) for c, v in cal.items()}
+        cal.clear()
         ctx = m.ctx
         run = lambda: ctx.run_async(m.in_ptrs, m.out_ptrs, sp)
-        r = {"tenants": list(configs.CONFIGS[cfg][0]), "ops": L}
-        if not a.no_calibrate:   # executor knobs (partition rule, claim depth) chosen by measurement
-            kn, med = m.calibrate()
+        if kn is not None:
             r["knobs"] = {"sm_partition_rule": kn[0], "claim_depth": kn[1], "steal": kn[2] if len(kn) > 2 else 2,
                           "calibration_us": {",".join(map(str, k)): round(v, 1) for k, v in med.items()}}
         for name, rho in (("all_concurrent", configs.all_concurrent_pointers(L)),
@@ -110,7 +126,7 @@ def main():
 
 def render_md(res):
     """Markdown table of a zoo_table JSON (profiles/<round>_zoo_table.md body)."""
-    rows = ["| mix | knobs (rule, D, steal) | all-conc. | rand | coord (P3,R2,M8) | seq sched. | SEQ | SEQ_G | MS_BFS | MS_G "
+    rows = ["| mix | CTAs/SM, knobs (rule, D, steal) | all-conc. | rand | coord (P3,R2,M8) | seq sched. | SEQ | SEQ_G | MS_BFS | MS_G "
             "| STAGE_EV | best vs SEQ_G | best vs MS_G | paper Seq / Stream / Ours-C |",
             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for cfg, r in res.items():
@@ -119,7 +135,7 @@ def render_md(res):
         pc = r.get("paper_context")
         paper = f"{pc['cudnn_seq_ms']} / {pc['stream_parallel_ms']} / {pc['ours_c_ms']} ({pc['table']})" if pc else "-"
         rows.append(
-            f"| {cfg}: {'+'.join(r['tenants'])} | {(kn['sm_partition_rule'], kn['claim_depth'], kn.get('steal', 2)) if kn else '(0, 0, 2)'} "
+            f"| {cfg}: {'+'.join(r['tenants'])} | {r.get('ctas_per_sm', 1)}, {(kn['sm_partition_rule'], kn['claim_depth'], kn.get('steal', 2)) if kn else '(0, 0, 2)'} "
             f"| {r['all_concurrent']:.3f} | {r['random_search']['ms']:.3f} | {r['coordinate_descent']['ms']:.3f} "
             f"| {r['sequential_schedule']:.3f} | {b['seq']:.3f} | {b['seq_graph']:.3f} | {b['ms_bfs']:.3f} "
             f"| {b['ms_graph']:.3f} | {b['stage_events']:.3f} | {min(b['seq'], b['seq_graph']) / r['best_executor_ms']:.2f}x "
