@@ -51,8 +51,12 @@ static constexpr int BN_MIN = 32;        // narrowest N tile the cost model cons
 #endif
 static int ring_slack(int st_boff) { return std::max(0, MT_BM * 128 - st_boff); }
 static int kgroup(int pipe, int st_bytes, int st_boff, int kb_per_split) {
+  // the co-resident configuration's 96 KB ring groups down to 2 stages (same box: c4 b1 689 ->
+  // 675 us, c3 639 -> 624 us; c4b8 unchanged); the 192 KB ring keeps >= 3 (2 measured neutral or
+  // slower there)
+  const int min_nst = pipe <= MT_PIPE_BYTES_2 ? 2 : MT_KG_MIN_NST;
   for (int kg = MT_KG_MAX; kg > 1; kg >>= 1)
-    if (kb_per_split >= 2 * kg && (pipe - ring_slack(st_boff)) / (kg * st_bytes) >= MT_KG_MIN_NST) return kg;
+    if (kb_per_split >= 2 * kg && (pipe - ring_slack(st_boff)) / (kg * st_bytes) >= min_nst) return kg;
   return 1;
 }
 static int ring_stages(int pipe, int st_bytes, int st_boff, int kg) {
