@@ -216,7 +216,10 @@ mt_status mt_sm_partition(mt_ctx *ctx, int32_t *sms);
  * tenant (FLOP/byte of the stage slice), slot 1 the same list reversed (f4 pairing). */
 mt_status mt_stage_homes(mt_ctx *ctx, int32_t *grid, int32_t *homes);
 
-/* Run the active schedule once on the persistent stage executor (one cooperative launch).
+/* Run the active schedule once on the persistent stage executor (one launch: cooperative with 1
+ * CTA/SM; with MT_OPT_CTAS_PER_SM = 2 a normal launch of a grid whose co-residency was checked by
+ * resource count at mt_set_option -- a CTA that could not become resident ends the run through the
+ * grid-barrier timeout with MT_ERR_INTERNAL).
  * inputs[N]: DEVICE fp32 NCHW graph inputs (may alias: the shared input of P:240).
  * outputs[N]: DEVICE fp32 [batch][out_c*out_h*out_w] (NHWC flatten; [batch][classes]).
  * stage_us[S] (host, may be NULL): device time of each stage (%globaltimer deltas).
