@@ -1979,7 +1979,7 @@ __device__ __forceinline__ uint32_t sm_id() {
 }
 
 template <bool F32>
-__global__ void __launch_bounds__(MT_NTHREADS, MT_PIPE_BYTES_1 / MT_PIPE_BYTES) executor_kernel(RunArgs a) {
+__global__ void __launch_bounds__(MT_NTHREADS, MT_CTAS_PER_SM) executor_kernel(RunArgs a) {
   uint8_t *smem = smem_base();
   __shared__ __align__(16) CtaShared sh;
   PipeState ps{0u, 0u, 0u};

@@ -12,17 +12,21 @@
 //    with a 96 KB ring, 255 registers per thread (2 x 128 x 256 = the whole register file) and 256
 //    TMEM columns (namespace mtk_cr).
 // The host plans with the values of the configuration the context runs (mt_ctx::dev).
+#define MT_PIPE_BYTES_1 (192 * 1024)   // ring of the 1-CTA-per-SM configuration (host planning)
+#ifndef MT_PIPE_BYTES_2
+#define MT_PIPE_BYTES_2 (96 * 1024)    // ring of the 2-CTA-per-SM configuration
+#endif
 #ifdef MT_CR
 #define MT_NTHREADS 128   // threads per CTA of every kernel
-#define MT_PIPE_BYTES (96 * 1024)    // shared-memory ring of the conv pipeline
+#define MT_PIPE_BYTES MT_PIPE_BYTES_2  // shared-memory ring of the conv pipeline
+#define MT_CTAS_PER_SM 2
 #define MT_NS mtk_cr
 #else
 #define MT_NTHREADS 256
-#define MT_PIPE_BYTES (192 * 1024)
+#define MT_PIPE_BYTES MT_PIPE_BYTES_1
+#define MT_CTAS_PER_SM 1
 #define MT_NS mtk
 #endif
-#define MT_PIPE_BYTES_1 (192 * 1024)   // ring of the 1-CTA-per-SM configuration (host planning)
-#define MT_PIPE_BYTES_2 (96 * 1024)    // ring of the 2-CTA-per-SM configuration
 #define MT_STAGES 4       // smem pipeline depth of the cp.async conv mainloop (32 KB stages)
 #define MT_MAXST 12       // max pipeline depth of the TMA conv mainloop (stage = A box + B box)
 #define MT_BM 128         // tcgen05 conv tile rows (output pixels), UMMA M
