@@ -25,6 +25,7 @@ ap.add_argument("--top", type=int, default=30)
 ap.add_argument("--partition", type=int, default=None)
 ap.add_argument("--steal", type=int, default=None)
 ap.add_argument("--claim", type=int, default=None)
+ap.add_argument("--cps", type=int, default=1, help="executor CTAs per SM (2: f4 co-resident build)")
 ap.add_argument("--synthetic", default=None, help="dwchain | pwchain | gapchain")
 a = ap.parse_args()
 if a.synthetic and a.synthetic.startswith("pw:"):
@@ -61,7 +62,7 @@ elif a.synthetic:
 else:
     g = configs.tenants(a.config)
 L = [x.n_ops for x in g]
-m = TenantMix(g)
+m = TenantMix(g, ctas_per_sm=a.cps)
 m.set_input(zoo.make_input(g[0]))
 rho = {"all_concurrent": configs.all_concurrent_pointers, "sequential": configs.sequential_pointers,
        "uniform4": configs.uniform_pointers}[a.schedule](L)
