@@ -130,3 +130,30 @@ def test_coresident_profile_batch_and_host_run():
     m.ctx.run_host([xh.data_ptr()] * len(L), [o.data_ptr() for o in outs_h])
     for a, b in zip(outs_h, ref):
         assert torch.equal(a, b.cpu())
+
+
+def test_coresident_stage_split_and_repeated_runs():
+    """one launch per stage (the profiling mode) in the co-resident configuration: the (slot, SM)
+    counters return to zero at every kernel exit, so every launch maps its CTAs again; outputs equal
+    the single launch's, and 20 back-to-back runs stay bit-identical"""
+    from paper_2111_14255_b200 import mt as M
+    m = mix("c3", 2)
+    L = [g.n_ops for g in m.graphs]
+    m.ctx.set_schedule_pointers(configs.uniform_pointers(L))
+    m.set_knobs((0, 0, 2))
+    m.run()
+    ref = _outs(m)
+    m.ctx.set_option(M.MT_OPT_STAGE_SPLIT, 1)
+    try:
+        for o in m.outputs:
+            o.zero_()
+        total, stages = m.run()
+        for a, b in zip(_outs(m), ref):
+            assert torch.equal(a, b)
+        assert len(stages) == 4 and all(s > 0 for s in stages)
+    finally:
+        m.ctx.set_option(M.MT_OPT_STAGE_SPLIT, 0)
+    for _ in range(20):
+        m.ctx.run_async(m.in_ptrs, m.out_ptrs)
+    for a, b in zip(_outs(m), ref):
+        assert torch.equal(a, b)
